@@ -1,0 +1,403 @@
+// qmb_gemm.cu -- tcgen05 kind::i8 GEMM (TMA -> smem -> UMMA -> TMEM -> fused
+// epilogue) and a warp-per-column dp4a GEMV path for skinny M (decode).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdio.h>
+#include <mutex>
+
+#include "qmb_gemm.cuh"
+
+namespace qmb {
+
+// ============================================================ tensor-core path
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 128;  // bytes of K per stage = one 128B swizzle atom
+constexpr int TC_THREADS = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
+
+template <int BN>
+struct TcCfg {
+  static constexpr int A_BYTES = TC_BM * TC_BK;
+  static constexpr int B_BYTES = BN * TC_BK;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
+  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                      int Kp, EpiParams ep) {
+  using C = TcCfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  const int num_m = (M + TC_BM - 1) / TC_BM;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_k = (Kp + TC_BK - 1) / TC_BK;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile / num_n) * TC_BM;
+        const int n0 = (tile % num_n) * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * TC_BK, m0);
+          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * TC_BK, n0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_i8(TC_BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int buf = it & 1;
+        const uint32_t use = (uint32_t)(it >> 1);
+        mbar_wait(&tempty[buf], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tbase + (uint32_t)(buf * BN);
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < TC_BK / 32; ++k) {
+            umma_i8(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    uint32_t err = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int buf = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      const int m0 = (tile / num_n) * TC_BM;
+      const int n0 = (tile % num_n) * BN;
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const long long m = (long long)m0 + row;
+      const uint32_t tcol = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tcol + c * 32, r);
+        const int nb = n0 + c * 32;
+        if (m < M && nb < N) {
+          const int s = find_seg(ep, nb);
+          const EpiSeg& sg = ep.seg[s];
+          const bool fast = (nb + 32 <= sg.n1) && (nb + 32 <= N) && ((sg.n0 & 15) == 0) && sg.bias == nullptr;
+          if (fast && sg.kind == EPI_F32) {
+            float* o = static_cast<float*>(sg.out) + m * sg.ld + (nb - sg.n0);
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              float4 v;
+              v.x = __fmul_rn(__int2float_rn((int)r[j + 0]), sg.acc_scale);
+              v.y = __fmul_rn(__int2float_rn((int)r[j + 1]), sg.acc_scale);
+              v.z = __fmul_rn(__int2float_rn((int)r[j + 2]), sg.acc_scale);
+              v.w = __fmul_rn(__int2float_rn((int)r[j + 3]), sg.acc_scale);
+              *reinterpret_cast<float4*>(o + j) = v;
+            }
+          } else if (fast && sg.kind == EPI_QUANT) {
+            int8_t* o = static_cast<int8_t*>(sg.out) + m * sg.ld + (nb - sg.n0);
+            uint32_t packed[8];
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              uint32_t w = 0;
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                float v = __fmul_rn(__int2float_rn((int)r[j + t]), sg.acc_scale);
+                int q = quant_i8(v, sg.out_div, ep.qmax, err);
+                w |= ((uint32_t)(q & 0xff)) << (8 * t);
+              }
+              packed[j / 4] = w;
+            }
+            *reinterpret_cast<uint4*>(o) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            *reinterpret_cast<uint4*>(o + 16) = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+          } else {
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+              const int n = nb + j;
+              if (n < N) epi_store_one(ep, ep.seg[find_seg(ep, n)], m, n, (int)r[j], err);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[buf]);
+    }
+    flag_error(ep.err, err);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, C::TMEM_COLS);
+  }
+}
+
+// ============================================================ SIMT GEMV path
+// One warp per output column n and a block of up to MB rows; lanes split K in
+// 16-byte slices; the int32 warp reduction is exact in any order.
+template <int MB>
+__global__ void __launch_bounds__(256) gemm_i8_simt_kernel(const int8_t* __restrict__ A, long long lda,
+                                                           const int8_t* __restrict__ Bt, long long ldb, int M,
+                                                           int N, int Kp, EpiParams ep, int vec) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = blockIdx.x * (blockDim.x >> 5) + warp;
+  const int m0 = blockIdx.y * MB;
+  if (n >= N) return;
+  int acc[MB];
+#pragma unroll
+  for (int i = 0; i < MB; ++i) acc[i] = 0;
+  const int8_t* brow = Bt + (long long)n * ldb;
+  if (vec) {
+    for (int k = lane * 16; k + 16 <= Kp; k += 32 * 16) {
+      const int4 b = __ldg(reinterpret_cast<const int4*>(brow + k));
+#pragma unroll
+      for (int i = 0; i < MB; ++i) {
+        if (m0 + i < M) {
+          const int4 a = __ldg(reinterpret_cast<const int4*>(A + (long long)(m0 + i) * lda + k));
+          acc[i] = __dp4a(a.x, b.x, acc[i]);
+          acc[i] = __dp4a(a.y, b.y, acc[i]);
+          acc[i] = __dp4a(a.z, b.z, acc[i]);
+          acc[i] = __dp4a(a.w, b.w, acc[i]);
+        }
+      }
+    }
+    for (int k = (Kp / 16) * 16 + lane; k < Kp; k += 32) {
+#pragma unroll
+      for (int i = 0; i < MB; ++i)
+        if (m0 + i < M) acc[i] += (int)A[(long long)(m0 + i) * lda + k] * (int)brow[k];
+    }
+  } else {
+    for (int k = lane; k < Kp; k += 32) {
+      const int b = brow[k];
+#pragma unroll
+      for (int i = 0; i < MB; ++i)
+        if (m0 + i < M) acc[i] += (int)A[(long long)(m0 + i) * lda + k] * b;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < MB; ++i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+  }
+  uint32_t err = 0;
+  const EpiSeg& sg = ep.seg[find_seg(ep, n)];
+#pragma unroll
+  for (int i = 0; i < MB; ++i) {
+    if (lane == i && m0 + i < M) epi_store_one(ep, sg, m0 + i, n, acc[i], err);
+  }
+  flag_error(ep.err, err);
+}
+
+// ============================================================ int8 tensor peak probe
+// One CTA per SM issues back-to-back M=128 x N=256 x K=32 kind::i8 MMAs on
+// resident smem operands (no TMA, no epilogue): the measured int8 dense peak
+// used as the roofline denominator for the GEMMs.
+__global__ void __launch_bounds__(128, 1) umma_i8_peak_kernel(int iters, int* sink) {
+  extern __shared__ uint8_t psm_raw[];
+  uint8_t* psm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(psm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t done_bar;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (128 + 256) * 128 / 4; i += blockDim.x) reinterpret_cast<int*>(psm)[i] = 0x01010101;
+  if (threadIdx.x == 0) {
+    mbar_init(&done_bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&tslot, 256);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t t = tslot;
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc = umma_idesc_i8(128, 256);
+    const uint32_t a0 = smem_u32(psm), b0 = smem_u32(psm + 128 * 128);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) umma_i8(t, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc, 1);
+    }
+    umma_commit(&done_bar);
+    mbar_wait(&done_bar, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(t, r);
+    if (threadIdx.x == 0) sink[blockIdx.x] = (int)r[0];
+    tmem_dealloc(t, 256);
+  }
+}
+
+// ============================================================ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+static bool make_tmap_i8(CUtensorMap* tm, const void* base, long long rows, long long cols, long long ld_bytes,
+                         int box_cols, int box_rows) {
+  auto enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)ld_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN>
+static cudaError_t launch_tc(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
+                             const EpiParams& ep, cudaStream_t st) {
+  using C = TcCfg<BN>;
+  CUtensorMap tmA, tmB;
+  if (!make_tmap_i8(&tmA, A, M, Kp, lda, TC_BK, TC_BM)) return cudaErrorInvalidValue;
+  if (!make_tmap_i8(&tmB, Bt, N, Kp, ldb, TC_BK, BN)) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  gemm_i8_tc_kernel<BN><<<grid, TC_THREADS, C::SMEM_BYTES, st>>>(tmA, tmB, M, N, Kp, ep);
+  return cudaGetLastError();
+}
+
+cudaError_t measure_i8_peak(int iters, double* tops) {
+  const int grid = num_sms();
+  int* sink = nullptr;
+  cudaError_t e = cudaMalloc(&sink, grid * sizeof(int));
+  if (e != cudaSuccess) return e;
+  const int smem = 1024 + (128 + 256) * 128;
+  cudaFuncSetAttribute(umma_i8_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  umma_i8_peak_kernel<<<grid, 128, smem>>>(iters / 4, sink);  // warm-up
+  cudaEventRecord(e0);
+  umma_i8_peak_kernel<<<grid, 128, smem>>>(iters, sink);
+  cudaEventRecord(e1);
+  e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *tops = 2.0 * 128.0 * 256.0 * 128.0 * (double)iters * grid / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e;
+}
+
+cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
+                    const EpiParams& ep, cudaStream_t st, int force_path) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  const bool tc_ok = (lda % 16 == 0) && (ldb % 16 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)Bt % 16 == 0) &&
+                     Kp > 0;
+  int path = force_path;
+  if (path == 0) path = (tc_ok && M > 16) ? 1 : 2;
+  if (path == 1 && !tc_ok) return cudaErrorInvalidValue;
+  if (path == 1) {
+    // Column tile: the largest BN that still gives >= 1 wave, else the smallest.
+    if (N <= 32) return launch_tc<32>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (N <= 64) return launch_tc<64>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (N <= 128) return launch_tc<128>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (N <= 192) return launch_tc<192>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    const long long m_tiles = (M + TC_BM - 1) / TC_BM;
+    if (m_tiles * ((N + 255) / 256) >= num_sms()) return launch_tc<256>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (m_tiles * ((N + 127) / 128) >= num_sms()) return launch_tc<128>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    return launch_tc<64>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+  }
+  const int vec = ((lda % 16) == 0 && (ldb % 16) == 0 && ((uintptr_t)A % 16) == 0 && ((uintptr_t)Bt % 16) == 0);
+  constexpr int MB = 8;
+  dim3 grid((N + 7) / 8, (M + MB - 1) / MB);
+  gemm_i8_simt_kernel<MB><<<grid, 256, 0, st>>>(A, lda, Bt, ldb, M, N, Kp, ep, vec);
+  return cudaGetLastError();
+}
+
+}  // namespace qmb

@@ -1,0 +1,72 @@
+// qmb_gemm.cuh -- int8 x int8 -> int32 GEMM for sm_100a with fused
+// dequant/requant epilogues (the reference's qlinear, qblock.py:98-123, and
+// the inline in_proj, qblock.py:192-198).
+//
+// C[m, n] = sum_k A[m, k] * Bt[n, k]      (A: [M, K] K-major, Bt: [N, K] K-major)
+// The int32 accumulator is exact, so any summation order matches numpy's
+// int32 matmul bit-for-bit; the epilogue then applies the reference's float
+// steps in the reference's order (int32 -> f32 RN, * f32 scale, + f32 bias,
+// optional softplus, quantize).
+#pragma once
+#include "qmb_common.cuh"
+
+namespace qmb {
+
+enum EpiKind : int {
+  EPI_QUANT = 0,     // int8 out = quantize(f32(acc) * s [+ bias])
+  EPI_F32 = 1,       // f32 out = f32(acc) * s [+ bias]
+  EPI_SOFTPLUS_Q = 2 // int8 out = quantize(softplus(f32(acc) * s [+ bias]))
+};
+
+struct EpiSeg {
+  int n0, n1;           // column range [n0, n1) of the GEMM output this segment covers
+  int kind;             // EpiKind
+  float acc_scale;      // f32(s_x * s_w * extra)
+  float out_div;        // f32(s_out) (quantizing kinds)
+  void* out;            // int8* or float*
+  long long ld;         // output row stride (elements)
+  const float* bias;    // per-column dequantized bias (indexed n - n0) or nullptr
+};
+
+struct EpiParams {
+  int nseg;
+  int qmax;
+  uint32_t* err;
+  EpiSeg seg[3];
+};
+
+__device__ __forceinline__ int find_seg(const EpiParams& ep, int n) {
+  int s = 0;
+#pragma unroll
+  for (int i = 1; i < 3; ++i)
+    if (i < ep.nseg && n >= ep.seg[i].n0) s = i;
+  return s;
+}
+
+// One output element, scalar path (shared by the SIMT kernel and ragged tiles).
+__device__ __forceinline__ void epi_store_one(const EpiParams& ep, const EpiSeg& sg, long long m, int n, int acc,
+                                              uint32_t& err) {
+  float v = __fmul_rn(__int2float_rn(acc), sg.acc_scale);
+  if (sg.bias) v = __fadd_rn(v, sg.bias[n - sg.n0]);
+  long long off = m * sg.ld + (n - sg.n0);
+  if (sg.kind == EPI_F32) {
+    static_cast<float*>(sg.out)[off] = v;
+  } else {
+    if (sg.kind == EPI_SOFTPLUS_Q) v = softplus_f32(v);
+    static_cast<int8_t*>(sg.out)[off] = (int8_t)quant_i8(v, sg.out_div, ep.qmax, err);
+  }
+}
+
+}  // namespace qmb
+
+// Host-side launcher API (implemented in qmb_gemm.cu).
+namespace qmb {
+// A: [M, Kp] with row stride lda bytes; Bt: [N, Kp] with row stride ldb bytes.
+// Requirements for the tensor-core path: lda % 16 == 0, ldb % 16 == 0, 16-byte
+// aligned base pointers.  Rows beyond M / N and K beyond Kp are zero-filled by TMA.
+cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
+                    const EpiParams& ep, cudaStream_t st, int force_path /*0 auto, 1 tc, 2 simt*/);
+int num_sms();
+// Dense int8 tensor-core throughput (TOP/s) of back-to-back 128x256x32 UMMAs on all SMs.
+cudaError_t measure_i8_peak(int iters, double* tops);
+}  // namespace qmb

@@ -1,0 +1,223 @@
+"""Quantized model loop -- mirror of `ssmq.model.forward_q` (pkg/src/ssmq/model.py:246-258)
+plus the batched, state-carrying prefill/decode engine the B200 path adds.
+
+The per-layer work (fused residual+RMSNorm+quant, block forward) runs in
+libqmb; the tied f32 LM head is a plain f32 GEMM (cuBLAS through torch, TF32
+off) and is tolerance-checked only.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .qblock import DeviceBlock, Mode, QuantizedBlock, device_block
+from .quant import is_device
+from .ssm import BlockConfig
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """model.py:32-72"""
+
+    vocab_size: int = 256
+    d_model: int = 64
+    n_layers: int = 2
+    expand: int = 2
+    d_state: int = 16
+    d_conv: int = 4
+    dt_rank: int = 4
+    bit_width: int = 8
+
+    def __post_init__(self):
+        if self.vocab_size <= 0 or self.n_layers <= 0:
+            raise ValueError("vocab_size and n_layers must be positive")
+        self.block
+
+    @property
+    def block(self) -> BlockConfig:
+        return BlockConfig(d_model=self.d_model, expand=self.expand, d_state=self.d_state, d_conv=self.d_conv,
+                           dt_rank=self.dt_rank)
+
+    @property
+    def d_inner(self) -> int:
+        return self.expand * self.d_model
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k in ("vocab_size", "d_model", "n_layers", "expand", "d_state", "d_conv",
+                                              "dt_rank", "bit_width")}
+
+
+@dataclass
+class QuantizedLayer:
+    norm_weight: object
+    block: QuantizedBlock
+
+
+@dataclass(eq=False)
+class QuantizedModel:
+    config: ModelConfig
+    mode: Mode
+    embedding: object
+    layers: list
+    final_norm: object
+    scales: object = None
+
+
+def _f32_dev(a) -> torch.Tensor:
+    return _device.to_device(a if is_device(a) else np.asarray(a, dtype=np.float32), torch.float32)
+
+
+class DeviceModel:
+    """Device-resident quantized model: embedding, norms and one libqmb block
+    handle per layer; batched prefill with optional state export, single-token
+    decode with carried (conv window, h) state, greedy generation."""
+
+    def __init__(self, model):
+        cfg = model.config
+        self.cfg = cfg
+        self.D = int(cfg.d_model)
+        self.V = int(cfg.vocab_size)
+        self.bits = int(cfg.bit_width)
+        self.embedding = _f32_dev(model.embedding)
+        self.final_norm = _f32_dev(model.final_norm)
+        self.norms = [_f32_dev(l.norm_weight) for l in model.layers]
+        self.s_in = [float(l.block.act["in"].scale) for l in model.layers]
+        self.blocks: list[DeviceBlock] = [device_block(l.block) for l in model.layers]
+        self._lib = _lib.load()
+
+    # ---------------------------------------------------------------- pieces
+    def _rmsnorm(self, x_out, x_res, res_out, gain, s_out, u_q, y_out, M, err, stream):
+        _lib.check(self._lib.qmb_rmsnorm_residual_quant(
+            x_out.data_ptr(), _device.ptr(x_res), _device.ptr(res_out), gain.data_ptr(), int(M), self.D,
+            float(s_out), self.bits, _device.ptr(u_q), _device.ptr(y_out), err.ptr, stream), "rmsnorm")
+
+    def embed(self, tokens: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        tok = tokens.reshape(-1).to(torch.int64)
+        out = out if out is not None else torch.empty((tok.numel(), self.D), dtype=torch.float32,
+                                                      device=tok.device)
+        _lib.check(self._lib.qmb_embed_gather(self.embedding.data_ptr(), tok.data_ptr(), tok.numel(), self.D,
+                                              out.data_ptr(), _device.stream_ptr()), "embed")
+        return out
+
+    def lm_head(self, final: torch.Tensor) -> torch.Tensor:
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
+        try:
+            return final @ self.embedding.T
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
+
+    # ---------------------------------------------------------------- prefill
+    def forward_hidden(self, tokens: torch.Tensor, *, states=None, scan_exp: int = 0, err=None):
+        """tokens [B, T] -> final-normed hidden [B*T, D] f32.  If `states` is a
+        list (one (conv, h) pair per layer, shaped for B), the prefill writes
+        the carried decode state into it."""
+        B, T = tokens.shape
+        M = B * T
+        stream = _device.stream_ptr()
+        err = err if err is not None else _device.err_flag()
+        x_out = self.embed(tokens)
+        x_res = torch.zeros_like(x_out)
+        u_q = torch.empty((M, self.D), dtype=torch.int8, device=x_out.device)
+        ws = _device.workspace(max(b.workspace_bytes(M) for b in self.blocks))
+        for li, blk in enumerate(self.blocks):
+            self._rmsnorm(x_out, x_res, x_res, self.norms[li], self.s_in[li], u_q, None, M, err, stream)
+            conv, h = states[li] if states is not None else (None, None)
+            blk.prefill(u_q, B, T, x_out, conv_state_out=conv, ssm_state_out=h, scan_exp=scan_exp, workspace=ws,
+                        err=err, stream=stream)
+        final = torch.empty_like(x_out)
+        self._rmsnorm(x_out, x_res, None, self.final_norm, 1.0, None, final, M, err, stream)
+        return final
+
+    def forward(self, tokens: torch.Tensor, *, last_only: bool = False, scan_exp: int = 0) -> torch.Tensor:
+        """Logits [B, T, V] (or [B, V] for the last position only)."""
+        B, T = tokens.shape
+        final = self.forward_hidden(tokens, scan_exp=scan_exp)
+        if last_only:
+            final = final.reshape(B, T, self.D)[:, -1]
+            return self.lm_head(final)
+        return self.lm_head(final).reshape(B, T, self.V)
+
+    # ---------------------------------------------------------------- decode
+    def new_states(self, B: int):
+        return [blk.new_state(B) for blk in self.blocks]
+
+    def prefill(self, tokens: torch.Tensor, states=None):
+        """Prompt prefill that also exports the decode state; returns
+        (last-position logits [B, V], states)."""
+        B, T = tokens.shape
+        states = states if states is not None else self.new_states(B)
+        final = self.forward_hidden(tokens, states=states)
+        return self.lm_head(final.reshape(B, T, self.D)[:, -1]), states
+
+    def decode_step(self, tokens: torch.Tensor, states, *, err=None, bufs=None) -> torch.Tensor:
+        """One token per sequence: tokens [B] -> logits [B, V]; states updated in place."""
+        B = tokens.shape[0]
+        stream = _device.stream_ptr()
+        err = err if err is not None else _device.err_flag()
+        if bufs is None:
+            bufs = self.decode_buffers(B)
+        x_out, x_res, u_q, final, ws = bufs
+        self.embed(tokens, out=x_out)
+        x_res.zero_()
+        for li, blk in enumerate(self.blocks):
+            self._rmsnorm(x_out, x_res, x_res, self.norms[li], self.s_in[li], u_q, None, B, err, stream)
+            conv, h = states[li]
+            blk.decode(u_q, conv, h, x_out, workspace=ws, err=err, stream=stream)
+        self._rmsnorm(x_out, x_res, None, self.final_norm, 1.0, None, final, B, err, stream)
+        return self.lm_head(final)
+
+    def decode_buffers(self, B: int):
+        dev = _device.device()
+        x_out = torch.empty((B, self.D), dtype=torch.float32, device=dev)
+        x_res = torch.empty_like(x_out)
+        u_q = torch.empty((B, self.D), dtype=torch.int8, device=dev)
+        final = torch.empty_like(x_out)
+        ws = torch.empty(max(b.workspace_bytes(B) for b in self.blocks), dtype=torch.uint8, device=dev)
+        return x_out, x_res, u_q, final, ws
+
+    def greedy_generate(self, prompt: torch.Tensor, steps: int) -> torch.Tensor:
+        """Greedy decoding with carried state (quantized analogue of
+        model.greedy_decode, model.py:364-379).  prompt [B, T] -> [B, T+steps]."""
+        logits, states = self.prefill(prompt)
+        out = [prompt]
+        bufs = self.decode_buffers(prompt.shape[0])
+        for s in range(steps):
+            nxt = torch.argmax(logits, dim=-1)
+            out.append(nxt[:, None])
+            if s + 1 < steps:
+                logits = self.decode_step(nxt, states, bufs=bufs)
+        _device.err_flag().raise_if_set()
+        return torch.cat(out, dim=1)
+
+
+def device_model(model) -> DeviceModel:
+    dm = model.__dict__.get("_qmb_device_model")
+    if dm is None:
+        dm = DeviceModel(model)
+        model.__dict__["_qmb_device_model"] = dm
+    return dm
+
+
+def forward_q(model, tokens):
+    """model.py:246-258: tokens (T,) -> logits (T, vocab) f32 (numpy in, numpy out)."""
+    as_numpy = not is_device(tokens)
+    tok = _device.to_device(np.asarray(tokens, dtype=np.int64) if as_numpy else tokens, torch.int64)
+    squeeze = tok.dim() == 1
+    if squeeze:
+        tok = tok[None]
+    logits = device_model(model).forward(tok)
+    _device.err_flag().raise_if_set()
+    if squeeze:
+        logits = logits[0]
+    return logits.cpu().numpy() if as_numpy else logits
+
+
+def forward(model, tokens, observer=None):
+    """model.py:261-266 (quantized models only on this path)."""
+    if observer is not None:
+        raise ValueError("observers attach to the float path only")
+    return forward_q(model, tokens)

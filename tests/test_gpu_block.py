@@ -1,0 +1,126 @@
+"""GPU block parity: every intermediate of block_forward_q, bit-exact against
+the reference's golden stage replay (tests/golden) and the oracle."""
+import numpy as np
+import pytest
+import torch
+
+from fixtures_util import BLOCK_FIXTURES, SMALL_BLOCKS, block_weights, load_block, mirror_block, oracle_block
+
+pytestmark = pytest.mark.gpu
+
+
+def _ws_views(dev, ws, M, meta):
+    lay = dev.workspace_layout(M)
+    E = meta["cfg"]["d_inner"]
+    N = meta["cfg"]["d_state"]
+    R = meta["cfg"]["dt_rank"]
+    Ep = (E + 15) // 16 * 16
+    Rp = (R + 15) // 16 * 16
+
+    def view(slot, dtype, cols, ld):
+        nbytes = torch.tensor([], dtype=dtype).element_size()
+        t = ws[lay[slot]:lay[slot] + M * ld * nbytes].view(dtype).reshape(M, ld)[:, :cols]
+        return t.cpu().numpy()
+
+    return dict(x_q=lambda: view("XQ", torch.int8, E, E), gated=lambda: view("Z", torch.float32, E, E),
+                scan_x=lambda: view("SCANX", torch.int8, E, Ep), b_q=lambda: view("B", torch.int8, N, N),
+                c_q=lambda: view("C", torch.int8, N, N), dtr_q=lambda: view("DTR", torch.int8, R, Rp),
+                delta_q=lambda: view("DELTA", torch.int8, E, E), y_q=lambda: view("YQ", torch.int8, E, Ep))
+
+
+@pytest.mark.parametrize("scan_exp", [0, 1])
+@pytest.mark.parametrize("name", BLOCK_FIXTURES)
+def test_block_prefill_stages_bit_exact(cuda, name, scan_exp):
+    from paper_2410_13229_b200 import _device
+    from paper_2410_13229_b200.qblock import device_block
+
+    z, meta = load_block(name)
+    w = block_weights(z, meta)
+    qb = mirror_block(z, meta, w)
+    dev = device_block(qb)
+    u = torch.from_numpy(z["u_q"]).cuda()
+    T = u.shape[0]
+    out = torch.empty((T, meta["cfg"]["d_model"]), dtype=torch.float32, device="cuda")
+    ws = torch.zeros(dev.workspace_bytes(T), dtype=torch.uint8, device="cuda")
+    E, N = meta["cfg"]["d_inner"], meta["cfg"]["d_state"]
+    K = meta["cfg"]["d_conv"]
+    conv_state = torch.zeros((1, K - 1, E), dtype=torch.int8, device="cuda")
+    h = torch.zeros((1, E, N), dtype=torch.float32, device="cuda")
+    dev.prefill(u, 1, T, out, u_scale=meta["u_scale"], conv_state_out=conv_state, ssm_state_out=h,
+                scan_exp=scan_exp, workspace=ws)
+    _device.err_flag().raise_if_set()
+    views = _ws_views(dev, ws, T, meta)
+    for stage in ("x_q", "scan_x", "b_q", "c_q", "dtr_q", "delta_q", "gated", "y_q"):
+        got = views[stage]()
+        ref = z[f"st_{stage}"]
+        if got.dtype.kind == "f":
+            ok = np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+        else:
+            ok = np.array_equal(got, ref)
+        assert ok, f"{name}: first mismatching stage {stage}: {np.count_nonzero(got != ref)} of {ref.size}"
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), z["st_out"].view(np.uint32)), f"{name}: out"
+    assert np.array_equal(h[0].cpu().numpy().view(np.uint32), z["st_h"].view(np.uint32)), f"{name}: final h"
+    ob = oracle_block(z, meta, w)
+    from oracle import oracle as o
+    st = o.block_stages(z["u_q"], meta["u_scale"], ob)
+    assert np.array_equal(conv_state[0].cpu().numpy(), st["conv_state"])
+
+
+@pytest.mark.parametrize("name", SMALL_BLOCKS)
+def test_block_forward_q_dropin_numpy(cuda, name):
+    """block_forward_q with numpy QTensors (the reference's calling convention)."""
+    from paper_2410_13229_b200 import QTensor, block_forward_q
+
+    z, meta = load_block(name)
+    qb = mirror_block(z, meta)
+    out = block_forward_q(QTensor(z["u_q"], meta["u_scale"]), qb)
+    assert isinstance(out, np.ndarray) and np.array_equal(out, z["st_out"])
+
+
+@pytest.mark.parametrize("name", ["m20_full", "p2_naive", "s130m"])
+def test_block_batched_sequences(cuda, oracle, name):
+    """B independent sequences in one launch equal B separate oracle runs."""
+    from paper_2410_13229_b200 import QTensor, block_forward_q
+
+    z, meta = load_block(name)
+    w = block_weights(z, meta)
+    qb = mirror_block(z, meta, w)
+    ob = oracle_block(z, meta, w)
+    rng = np.random.default_rng(5)
+    B, T, D = 3, 21, meta["cfg"]["d_model"]
+    u = rng.integers(-127, 128, size=(B, T, D)).astype(np.int8)
+    got = block_forward_q(QTensor(u, meta["u_scale"]), qb)
+    for b in range(B):
+        ref = oracle.block_forward_q(u[b], meta["u_scale"], ob)
+        assert np.array_equal(got[b], ref), b
+
+
+@pytest.mark.parametrize("name", ["tiny_full", "m12_full", "p2_inper", "s2p8b"])
+def test_block_decode_equals_prefill(cuda, name):
+    """Prefill k tokens (exporting state), then decode the rest one by one: every
+    decoded row and the final state equal the one-shot prefill bit-for-bit."""
+    from paper_2410_13229_b200 import _device
+    from paper_2410_13229_b200.qblock import device_block
+
+    z, meta = load_block(name)
+    qb = mirror_block(z, meta)
+    dev = device_block(qb)
+    u = torch.from_numpy(z["u_q"]).cuda()
+    T, D = u.shape
+    B = 2
+    ub = u[None].repeat(B, 1, 1).contiguous()
+    k = T // 2
+    conv, h = dev.new_state(B)
+    pre = torch.empty((B * k, D), dtype=torch.float32, device="cuda")
+    dev.prefill(ub[:, :k].contiguous().reshape(B * k, D), B, k, pre, u_scale=meta["u_scale"], conv_state_out=conv,
+                ssm_state_out=h)
+    rows = [pre.reshape(B, k, D)]
+    for t in range(k, T):
+        o = torch.empty((B, D), dtype=torch.float32, device="cuda")
+        dev.decode(ub[:, t].contiguous(), conv, h, o, u_scale=meta["u_scale"])
+        rows.append(o[:, None])
+    _device.err_flag().raise_if_set()
+    got = torch.cat(rows, dim=1).cpu().numpy()
+    for b in range(B):
+        assert np.array_equal(got[b].view(np.uint32), z["st_out"].view(np.uint32)), b
+    assert np.array_equal(h[0].cpu().numpy().view(np.uint32), z["st_h"].view(np.uint32))

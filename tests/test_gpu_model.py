@@ -1,0 +1,79 @@
+"""GPU model-level parity: forward_q logits (tolerance; the tied f32 LM head is
+a BLAS GEMM on both sides), final hidden states (bit-exact), per-layer
+activations (bit-exact) and greedy decoding with carried state."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_npz
+from fixtures_util import mirror_model, oracle_model
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_RTOL = 1e-5  # max|dlogit| <= 1e-5 * max|logit|
+
+
+@pytest.mark.parametrize("name", ["tiny2", "config1"])
+def test_forward_q_matches_reference(cuda, oracle, name):
+    from paper_2410_13229_b200 import forward_q
+    from paper_2410_13229_b200.model import device_model
+
+    z, meta = load_npz(f"model_{name}.npz")
+    qm = mirror_model(z, meta)
+    tokens = z["tokens"]
+    logits = forward_q(qm, tokens)
+    ref = z["logits"]
+    assert logits.shape == ref.shape
+    assert np.max(np.abs(logits - ref)) <= LOGIT_RTOL * np.max(np.abs(ref))
+    # bit-exact hidden state vs the oracle replay of the reference
+    om = oracle_model(z, meta)
+    hid_ref = oracle.forward_hidden(om, tokens)
+    hid = device_model(qm).forward_hidden(torch.from_numpy(tokens).cuda()[None]).cpu().numpy()
+    assert np.array_equal(hid, hid_ref)
+
+
+def test_batched_prefill_last_logits(cuda, oracle):
+    from paper_2410_13229_b200.model import device_model
+
+    z, meta = load_npz("model_tiny2.npz")
+    qm = mirror_model(z, meta)
+    om = oracle_model(z, meta)
+    rng = np.random.default_rng(9)
+    toks = rng.integers(0, meta["config"]["vocab_size"], size=(4, 30))
+    dm = device_model(qm)
+    last = dm.forward(torch.from_numpy(toks).cuda(), last_only=True).cpu().numpy()
+    for b in range(4):
+        ref = oracle.forward_q(om, toks[b])[-1]
+        assert np.max(np.abs(last[b] - ref)) <= LOGIT_RTOL * np.max(np.abs(ref))
+
+
+def test_greedy_decode_matches_oracle(cuda, oracle):
+    from paper_2410_13229_b200.model import device_model
+
+    z, meta = load_npz("model_tiny2.npz")
+    qm = mirror_model(z, meta)
+    om = oracle_model(z, meta)
+    prompt = z["tokens"][:16]
+    steps = 12
+    ref = oracle.greedy(om, prompt, steps)
+    got = device_model(qm).greedy_generate(torch.from_numpy(prompt).cuda()[None].repeat(2, 1), steps).cpu().numpy()
+    for b in range(2):
+        assert got[b].tolist() == ref, (got[b].tolist(), ref)
+
+
+def test_decode_hidden_bit_exact(cuda, oracle):
+    """Decode-step hidden states equal the one-shot prefill rows bit-for-bit."""
+    from paper_2410_13229_b200.model import device_model
+
+    z, meta = load_npz("model_tiny2.npz")
+    qm = mirror_model(z, meta)
+    dm = device_model(qm)
+    tokens = torch.from_numpy(z["tokens"][:24]).cuda()[None]
+    full = dm.forward_hidden(tokens).cpu().numpy()
+    states = dm.new_states(1)
+    dm.forward_hidden(tokens[:, :10], states=states)
+    bufs = dm.decode_buffers(1)
+    for t in range(10, 24):
+        dm.decode_step(tokens[:, t], states, bufs=bufs)
+        hidden = bufs[3].cpu().numpy()[0]
+        assert np.array_equal(hidden, full[t]), t
