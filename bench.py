@@ -209,6 +209,14 @@ def run_ours(args):
         step(tokens)
     torch.cuda.synchronize()
     _device.err_flag().raise_if_set()
+    if args.ncu:
+        # one profiled step between cudaProfilerStart/Stop (ncu --profile-from-start off)
+        torch.cuda.profiler.start()
+        step(tokens)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        print(json.dumps({"ncu_step": "done", "config": args.config, "batch": B, "seq": T}), flush=True)
+        return
 
     def timed(fn, n):
         if world > 1:
@@ -338,6 +346,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--calib-tokens", type=int, default=256)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="profile one prefill step (ncu --profile-from-start off)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

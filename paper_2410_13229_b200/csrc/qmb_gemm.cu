@@ -141,7 +141,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (m < M && nb < N) {
           const int s = find_seg(ep, nb);
           const EpiSeg& sg = ep.seg[s];
-          const bool fast = (nb + 32 <= sg.n1) && (nb + 32 <= N) && ((sg.n0 & 15) == 0) && sg.bias == nullptr;
+          const long long ldb_bytes = sg.ld * (sg.kind == EPI_F32 ? 4 : 1);
+          const bool fast = (nb + 32 <= sg.n1) && (nb + 32 <= N) && ((sg.n0 & 15) == 0) && sg.bias == nullptr &&
+                            (ldb_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(sg.out) & 15) == 0);
           if (fast && sg.kind == EPI_F32) {
             float* o = static_cast<float*>(sg.out) + m * sg.ld + (nb - sg.n0);
 #pragma unroll
