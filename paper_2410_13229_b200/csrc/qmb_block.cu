@@ -72,6 +72,7 @@ struct qmb_block {
   float* d_deq;     // [E]
   int8_t* w_out_t;  // [D, Ep]
   float* luts;      // [4][256] dequant tables: x, dt, b, c (index q + 128)
+  float* sp_qtab;   // [QTAB_FLOATS] verified softplus+quantize thresholds for dt_proj
 };
 
 extern "C" int qmb_abi_version(void) { return QMB_ABI_VERSION; }
@@ -205,7 +206,8 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
   const size_t o_win = take(w_in_t.size()), o_cw = take((size_t)Kc * E), o_cb = take(E * 4), o_wx = take(w_x_t.size()),
                o_wdt = take(w_dt_t.size()), o_dtb = take(E * 4), o_a = take((size_t)E * N * 4),
                o_acol = take((size_t)E * N), o_lut = take((size_t)128 * b->exp_ncols * 4), o_d = take(E * 4),
-               o_wo = take(w_out_t.size()), o_luts = take(4 * 256 * 4), o_avals = take(a_vals.size() * 4);
+               o_wo = take(w_out_t.size()), o_luts = take(4 * 256 * 4), o_avals = take(a_vals.size() * 4),
+               o_qtab = take(QTAB_FLOATS * 4), o_scr = take(16);
   cudaError_t e = cudaMalloc(&b->mem, off);
   if (e != cudaSuccess) {
     delete b;
@@ -225,6 +227,8 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
   b->w_out_t = (int8_t*)(base + o_wo);
   b->luts = (float*)(base + o_luts);
   float* avals_dev = (float*)(base + o_avals);
+  b->sp_qtab = (float*)(base + o_qtab);
+  uint32_t* scratch = (uint32_t*)(base + o_scr);
   struct Up {
     void* dst;
     const void* src;
@@ -246,6 +250,7 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
     }
   }
   e = build_exp_lut(b->luts + 256, avals_dev, b->exp_ncols, b->exp_lut, 0);
+  if (e == cudaSuccess) e = build_softplus_qtab(f32(d->act[QMB_ACT_DT]), b->qmax, b->sp_qtab, scratch, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     cudaFree(b->mem);
@@ -397,7 +402,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     ep.qmax = b->qmax;
     ep.err = err;
     ep.seg[0] = EpiSeg{0, E, EPI_SOFTPLUS_Q, f32(b->act[QMB_ACT_DT_R] * b->s_w_dt * 1.0), f32(b->act[QMB_ACT_DT]),
-                       delta, E, b->dt_bias};
+                       delta, E, b->dt_bias, b->sp_qtab};
     QMB_CUDA(gemm_i8(dtr, b->Rp, b->w_dt_t, b->Rp, (int)M, E, R, ep, st, 0), "dt_proj gemm");
   }
   // scan + D skip + gate (qblock.py:207-210), gated y written over z

@@ -12,7 +12,8 @@ namespace qmb {
 // ============================================================ tensor-core path
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 128;  // bytes of K per stage = one 128B swizzle atom
-constexpr int TC_THREADS = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
+constexpr int TC_EPI_WARPS = 8;   // two warps per TMEM lane quarter, each owning half the columns
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;  // warp0 TMA, warp1 MMA, warps 2.. epilogue
 
 template <int BN>
 struct TcCfg {
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 32 * TC_EPI_WARPS);
     }
     fence_barrier_init();
   }
@@ -120,8 +121,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int quarter = warp & 3;           // TMEM lane quarter this warp may access
+    const int half = (warp - 2) / 4;        // which half of the tile's column chunks
     const int row = quarter * 32 + lane;
+    constexpr int CHUNKS = BN / 32;
+    constexpr int CH_PER = (CHUNKS + 1) / 2;
     uint32_t err = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const long long m = (long long)m0 + row;
       const uint32_t tcol = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * CH_PER; c < CHUNKS && c < (half + 1) * CH_PER; ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tcol + c * 32, r);
         const int nb = n0 + c * 32;
@@ -142,37 +146,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int s = find_seg(ep, nb);
           const EpiSeg& sg = ep.seg[s];
           const long long ldb_bytes = sg.ld * (sg.kind == EPI_F32 ? 4 : 1);
-          const bool fast = (nb + 32 <= sg.n1) && (nb + 32 <= N) && ((sg.n0 & 15) == 0) && sg.bias == nullptr &&
+          const bool fast = (nb + 32 <= sg.n1) && (nb + 32 <= N) && ((sg.n0 & 15) == 0) &&
                             (ldb_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(sg.out) & 15) == 0);
-          if (fast && sg.kind == EPI_F32) {
-            float* o = static_cast<float*>(sg.out) + m * sg.ld + (nb - sg.n0);
+          if (fast) {
+            float v[32];
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              float4 v;
-              v.x = __fmul_rn(__int2float_rn((int)r[j + 0]), sg.acc_scale);
-              v.y = __fmul_rn(__int2float_rn((int)r[j + 1]), sg.acc_scale);
-              v.z = __fmul_rn(__int2float_rn((int)r[j + 2]), sg.acc_scale);
-              v.w = __fmul_rn(__int2float_rn((int)r[j + 3]), sg.acc_scale);
-              *reinterpret_cast<float4*>(o + j) = v;
-            }
-          } else if (fast && sg.kind == EPI_QUANT) {
-            int8_t* o = static_cast<int8_t*>(sg.out) + m * sg.ld + (nb - sg.n0);
-            uint32_t packed[8];
+            for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__int2float_rn((int)r[j]), sg.acc_scale);
+            if (sg.bias) {
+              const float4* bp = reinterpret_cast<const float4*>(sg.bias + (nb - sg.n0));
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              uint32_t w = 0;
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                float v = __fmul_rn(__int2float_rn((int)r[j + t]), sg.acc_scale);
-                int q = quant_i8(v, sg.out_div, ep.qmax, err);
-                w |= ((uint32_t)(q & 0xff)) << (8 * t);
+              for (int j = 0; j < 32; j += 4) {
+                const float4 bb = __ldg(bp + j / 4);
+                v[j] = __fadd_rn(v[j], bb.x);
+                v[j + 1] = __fadd_rn(v[j + 1], bb.y);
+                v[j + 2] = __fadd_rn(v[j + 2], bb.z);
+                v[j + 3] = __fadd_rn(v[j + 3], bb.w);
               }
-              packed[j / 4] = w;
             }
-            *reinterpret_cast<uint4*>(o) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-            *reinterpret_cast<uint4*>(o + 16) = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+            if (sg.kind == EPI_F32) {
+              float4* o = reinterpret_cast<float4*>(static_cast<float*>(sg.out) + m * sg.ld + (nb - sg.n0));
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) o[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {
+              uint32_t packed[8];
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  const int q = sg.kind == EPI_SOFTPLUS_Q ? softplus_quant(v[j + t], sg.qtab, sg.out_div, ep.qmax, err)
+                                                          : quant_i8(v[j + t], sg.out_div, ep.qmax, err);
+                  w |= ((uint32_t)(q & 0xff)) << (8 * t);
+                }
+                packed[j / 4] = w;
+              }
+              uint4* o = reinterpret_cast<uint4*>(static_cast<int8_t*>(sg.out) + m * sg.ld + (nb - sg.n0));
+              o[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+              o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+            }
           } else {
-#pragma unroll 4
+#pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int n = nb + j;
               if (n < N) epi_store_one(ep, ep.seg[find_seg(ep, n)], m, n, (int)r[j], err);

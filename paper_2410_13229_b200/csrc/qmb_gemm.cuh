@@ -26,7 +26,30 @@ struct EpiSeg {
   void* out;            // int8* or float*
   long long ld;         // output row stride (elements)
   const float* bias;    // per-column dequantized bias (indexed n - n0) or nullptr
+  const float* qtab;    // EPI_SOFTPLUS_Q: verified threshold table (softplus_qtab) or nullptr
 };
+
+// Verified threshold table for a monotone-in-practice quantized function
+// q(v) = quantize(f(v)): th[k-1] = min{v : q(v) >= k} (k = 1..127, +inf pad),
+// th[128..129] = [lo, hi] interval of v where the table was found (by an
+// exhaustive sweep over all 2^32 floats at handle creation) to disagree with
+// the exact evaluation; there the exact formula is used.  Exact by construction.
+constexpr int QTAB_FLOATS = 130;
+
+__device__ __forceinline__ int qtab_count(const float* __restrict__ th, float v) {
+  int idx = 0;
+#pragma unroll
+  for (int step = 64; step >= 1; step >>= 1)
+    if (v >= __ldg(th + idx + step - 1)) idx += step;
+  return idx;
+}
+
+__device__ __forceinline__ int softplus_quant(float v, const float* __restrict__ qtab, float s_div, int qmax,
+                                              uint32_t& err) {
+  if (qtab && fabsf(v) <= 3.402823466e38f && !(v >= __ldg(qtab + 128) && v <= __ldg(qtab + 129)))
+    return qtab_count(qtab, v);
+  return quant_i8(softplus_f32(v), s_div, qmax, err);
+}
 
 struct EpiParams {
   int nseg;
@@ -51,8 +74,9 @@ __device__ __forceinline__ void epi_store_one(const EpiParams& ep, const EpiSeg&
   long long off = m * sg.ld + (n - sg.n0);
   if (sg.kind == EPI_F32) {
     static_cast<float*>(sg.out)[off] = v;
+  } else if (sg.kind == EPI_SOFTPLUS_Q) {
+    static_cast<int8_t*>(sg.out)[off] = (int8_t)softplus_quant(v, sg.qtab, sg.out_div, ep.qmax, err);
   } else {
-    if (sg.kind == EPI_SOFTPLUS_Q) v = softplus_f32(v);
     static_cast<int8_t*>(sg.out)[off] = (int8_t)quant_i8(v, sg.out_div, ep.qmax, err);
   }
 }

@@ -91,6 +91,10 @@ cudaError_t selective_scan(const ScanParams& p, int use_lut, cudaStream_t st);
 // exp_lut[r * ncols + c] = glibc_expf(lut_dt[r + 128] * a_vals[c]) for r in [0, 127]
 cudaError_t build_exp_lut(const float* lut_dt, const float* a_vals, int ncols, float* exp_lut, cudaStream_t st);
 
+// Verified softplus+quantize threshold table (QTAB_FLOATS floats at `tab`);
+// scratch2: 2 device uint32 words.  Enqueued on `st` (the sweep covers all 2^32 floats).
+cudaError_t build_softplus_qtab(float s_div, int qmax, float* tab, uint32_t* scratch2, cudaStream_t st);
+
 // ---------------------------------------------------------------- misc
 cudaError_t transpose_i8(const int8_t* src, long long rows, long long cols, long long lds, int8_t* dst,
                          long long ldd, cudaStream_t st);  // dst[c, r] = src[r, c]
