@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdio.h>
+#include <string.h>
 #include <mutex>
 
 #include "qmb_gemm.cuh"
@@ -10,32 +11,44 @@
 namespace qmb {
 
 // ============================================================ tensor-core path
+// Persistent warp-specialized kernel: warp 0 = TMA producer, warp 1 = TMEM
+// allocator + single-thread UMMA issuer, EPIW epilogue warps (EPIW/4 per TMEM
+// lane quarter, splitting the tile's 32-column chunks).  The accumulator is
+// double-buffered in TMEM so the epilogue of tile i overlaps the MMAs of tile
+// i+1.  With TMAOUT, the f32 segment is staged through swizzled shared memory
+// (32 rows x 16 floats per store) and written with TMA bulk tensor stores.
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 128;  // bytes of K per stage = one 128B swizzle atom
-constexpr int TC_EPI_WARPS = 8;   // two warps per TMEM lane quarter, each owning half the columns
-constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;  // warp0 TMA, warp1 MMA, warps 2.. epilogue
 
-template <int BN>
+template <int BN, int EPIW, bool TMAOUT>
 struct TcCfg {
+  static constexpr int THREADS = 64 + 32 * EPIW;
   static constexpr int A_BYTES = TC_BM * TC_BK;
   static constexpr int B_BYTES = BN * TC_BK;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
-  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16;
+  static constexpr int STG_BYTES = TMAOUT ? EPIW * 4096 : 0;  // 2 x (32 rows x 64 B) per epilogue warp
+  static constexpr int BUDGET = 230 * 1024 - 1024 - STG_BYTES - 1024;
+  static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
+  static constexpr int TMEM_COLS =
+      (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int SMEM_BYTES =
+      1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + QTAB_FLOATS * 4 + (2 * STAGES + 4) * 8 + 16;
+  static_assert(STAGES >= 2, "pipeline too shallow");
 };
 
-template <int BN>
-__global__ void __launch_bounds__(TC_THREADS, 1)
-    gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                      int Kp, EpiParams ep) {
-  using C = TcCfg<BN>;
+template <int BN, int EPIW, bool TMAOUT>
+__global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
+    gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmC, int M, int N, int Kp, EpiParams ep) {
+  using C = TcCfg<BN, EPIW, TMAOUT>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint8_t* sStg = smem + STAGES * C::STAGE_BYTES;  // 1024-aligned
+  float* sQtab = reinterpret_cast<float*>(sStg + C::STG_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sQtab + QTAB_FLOATS + 2);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -47,16 +60,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (TMAOUT) tma_prefetch_desc(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 32 * TC_EPI_WARPS);
+      mbar_init(&tempty[b], 32 * EPIW);
     }
     fence_barrier_init();
   }
+  // softplus threshold table of the (single) EPI_SOFTPLUS_Q segment -> smem
+  const float* qtab_g = nullptr;
+  for (int s = 0; s < ep.nseg; ++s)
+    if (ep.seg[s].kind == EPI_SOFTPLUS_Q) qtab_g = ep.seg[s].qtab;
+  if (qtab_g)
+    for (int k = threadIdx.x; k < QTAB_FLOATS; k += blockDim.x) sQtab[k] = qtab_g[k];
   if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
@@ -121,11 +141,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int quarter = warp & 3;           // TMEM lane quarter this warp may access
-    const int half = (warp - 2) / 4;        // which half of the tile's column chunks
+    const int ew = warp - 2;                 // epilogue warp index
+    const int quarter = warp & 3;            // TMEM lane quarter this warp may access
+    const int part = ew / 4;                 // which 1/(EPIW/4) slice of the column chunks
+    constexpr int PARTS = EPIW / 4;
     const int row = quarter * 32 + lane;
     constexpr int CHUNKS = BN / 32;
-    constexpr int CH_PER = (CHUNKS + 1) / 2;
+    constexpr int CH_PER = (CHUNKS + PARTS - 1) / PARTS;
+    float* stg = reinterpret_cast<float*>(sStg + (TMAOUT ? ew * 4096 : 0));
+    const float* qtab = qtab_g ? sQtab : nullptr;
     uint32_t err = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
@@ -138,57 +162,98 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const long long m = (long long)m0 + row;
       const uint32_t tcol = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN);
 #pragma unroll 1
-      for (int c = half * CH_PER; c < CHUNKS && c < (half + 1) * CH_PER; ++c) {
+      for (int c = part * CH_PER; c < CHUNKS && c < (part + 1) * CH_PER; ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tcol + c * 32, r);
         const int nb = n0 + c * 32;
-        if (m < M && nb < N) {
-          const int s = find_seg(ep, nb);
-          const EpiSeg& sg = ep.seg[s];
-          const long long ldb_bytes = sg.ld * (sg.kind == EPI_F32 ? 4 : 1);
-          const bool fast = (nb + 32 <= sg.n1) && (nb + 32 <= N) && ((sg.n0 & 15) == 0) &&
-                            (ldb_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(sg.out) & 15) == 0);
-          if (fast) {
-            float v[32];
+        if (nb >= N) continue;  // warp-uniform
+        const int s = find_seg(ep, nb);
+        const EpiSeg& sg = ep.seg[s];
+        if (TMAOUT && s == ep.tma_seg && nb + 32 <= sg.n1 && nb + 32 <= N) {
+          // f32 tile rows through swizzled smem -> TMA store (rows >= M are clipped by TMA)
+          float v[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__int2float_rn((int)r[j]), sg.acc_scale);
-            if (sg.bias) {
-              const float4* bp = reinterpret_cast<const float4*>(sg.bias + (nb - sg.n0));
+          for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__int2float_rn((int)r[j]), sg.acc_scale);
+          if (sg.bias) {
 #pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                const float4 bb = __ldg(bp + j / 4);
-                v[j] = __fadd_rn(v[j], bb.x);
-                v[j + 1] = __fadd_rn(v[j + 1], bb.y);
-                v[j + 2] = __fadd_rn(v[j + 2], bb.z);
-                v[j + 3] = __fadd_rn(v[j + 3], bb.w);
-              }
+            for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(v[j], __ldg(sg.bias + (nb - sg.n0) + j));
+          }
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float* hb = stg + h * 512;  // 32 rows x 16 floats, 64B rows, SWIZZLE_64B
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int pos = q ^ ((lane >> 1) & 3);
+              *reinterpret_cast<float4*>(hb + lane * 16 + pos * 4) =
+                  make_float4(v[h * 16 + q * 4], v[h * 16 + q * 4 + 1], v[h * 16 + q * 4 + 2], v[h * 16 + q * 4 + 3]);
             }
-            if (sg.kind == EPI_F32) {
-              float4* o = reinterpret_cast<float4*>(static_cast<float*>(sg.out) + m * sg.ld + (nb - sg.n0));
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, stg, nb - sg.n0, m0 + quarter * 32);
+            tma_store_2d(&tmC, stg + 512, nb - sg.n0 + 16, m0 + quarter * 32);
+            bulk_commit();
+          }
+          continue;
+        }
+        if (m >= M) continue;
+        const long long ldb_bytes = sg.ld * (sg.kind == EPI_F32 ? 4 : 1);
+        const bool fast = (nb + 32 <= sg.n1) && (nb + 32 <= N) && ((sg.n0 & 15) == 0) && (ldb_bytes % 16 == 0) &&
+                          ((reinterpret_cast<uintptr_t>(sg.out) & 15) == 0);
+        if (fast) {
+          float v[32];
 #pragma unroll
-              for (int j = 0; j < 32; j += 4) o[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            } else {
-              uint32_t packed[8];
+          for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__int2float_rn((int)r[j]), sg.acc_scale);
+          if (sg.bias) {
+            const float4* bp = reinterpret_cast<const float4*>(sg.bias + (nb - sg.n0));
 #pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                uint32_t w = 0;
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                  const int q = sg.kind == EPI_SOFTPLUS_Q ? softplus_quant(v[j + t], sg.qtab, sg.out_div, ep.qmax, err)
-                                                          : quant_i8(v[j + t], sg.out_div, ep.qmax, err);
-                  w |= ((uint32_t)(q & 0xff)) << (8 * t);
-                }
-                packed[j / 4] = w;
-              }
-              uint4* o = reinterpret_cast<uint4*>(static_cast<int8_t*>(sg.out) + m * sg.ld + (nb - sg.n0));
-              o[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-              o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+            for (int j = 0; j < 32; j += 4) {
+              const float4 bb = __ldg(bp + j / 4);
+              v[j] = __fadd_rn(v[j], bb.x);
+              v[j + 1] = __fadd_rn(v[j + 1], bb.y);
+              v[j + 2] = __fadd_rn(v[j + 2], bb.z);
+              v[j + 3] = __fadd_rn(v[j + 3], bb.w);
             }
+          }
+          if (sg.kind == EPI_F32) {
+            float4* o = reinterpret_cast<float4*>(static_cast<float*>(sg.out) + m * sg.ld + (nb - sg.n0));
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) o[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
           } else {
+            uint32_t packed[8];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int n = nb + j;
-              if (n < N) epi_store_one(ep, ep.seg[find_seg(ep, n)], m, n, (int)r[j], err);
+            for (int j = 0; j < 32; j += 4) {
+              uint32_t w = 0;
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const int q = sg.kind == EPI_SOFTPLUS_Q ? softplus_quant(v[j + t], qtab, sg.out_div, ep.qmax, err)
+                                                        : quant_i8(v[j + t], sg.out_div, ep.qmax, err);
+                w |= ((uint32_t)(q & 0xff)) << (8 * t);
+              }
+              packed[j / 4] = w;
+            }
+            uint4* o = reinterpret_cast<uint4*>(static_cast<int8_t*>(sg.out) + m * sg.ld + (nb - sg.n0));
+            o[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int n = nb + j;
+            if (n < N) {
+              const EpiSeg& sj = ep.seg[find_seg(ep, n)];
+              float v = __fmul_rn(__int2float_rn((int)r[j]), sj.acc_scale);
+              if (sj.bias) v = __fadd_rn(v, sj.bias[n - sj.n0]);
+              const long long off = m * sj.ld + (n - sj.n0);
+              if (sj.kind == EPI_F32)
+                static_cast<float*>(sj.out)[off] = v;
+              else
+                static_cast<int8_t*>(sj.out)[off] =
+                    (int8_t)(sj.kind == EPI_SOFTPLUS_Q ? softplus_quant(v, qtab, sj.out_div, ep.qmax, err)
+                                                       : quant_i8(v, sj.out_div, ep.qmax, err));
             }
           }
         }
@@ -196,6 +261,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_before();
       mbar_arrive(&tempty[buf]);
     }
+    if (TMAOUT && lane == 0) bulk_wait0();
     flag_error(ep.err, err);
   }
 
@@ -344,24 +410,61 @@ int num_sms() {
   return n;
 }
 
-template <int BN>
+static bool make_tmap_f32_store(CUtensorMap* tm, const void* base, long long rows, long long cols, long long ld_bytes) {
+  auto enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)ld_bytes};
+  cuuint32_t box[2] = {16, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int EPIW, bool TMAOUT>
 static cudaError_t launch_tc(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
-                             const EpiParams& ep, cudaStream_t st) {
-  using C = TcCfg<BN>;
-  CUtensorMap tmA, tmB;
+                             EpiParams ep, cudaStream_t st) {
+  using C = TcCfg<BN, EPIW, TMAOUT>;
+  CUtensorMap tmA, tmB, tmC;
   if (!make_tmap_i8(&tmA, A, M, Kp, lda, TC_BK, TC_BM)) return cudaErrorInvalidValue;
   if (!make_tmap_i8(&tmB, Bt, N, Kp, ldb, TC_BK, BN)) return cudaErrorInvalidValue;
+  memset(&tmC, 0, sizeof(tmC));
+  if (TMAOUT) {
+    const EpiSeg& s = ep.seg[ep.tma_seg];
+    if (!make_tmap_f32_store(&tmC, s.out, M, s.n1 - s.n0, s.ld * 4)) return cudaErrorInvalidValue;
+  } else {
+    ep.tma_seg = -1;
+  }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc_kernel<BN, EPIW, TMAOUT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_i8_tc_kernel<BN><<<grid, TC_THREADS, C::SMEM_BYTES, st>>>(tmA, tmB, M, N, Kp, ep);
+  gemm_i8_tc_kernel<BN, EPIW, TMAOUT><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(tmA, tmB, tmC, M, N, Kp, ep);
   return cudaGetLastError();
+}
+
+template <int BN>
+static cudaError_t launch_tc_bn(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
+                                EpiParams ep, cudaStream_t st) {
+  bool heavy = false;
+  ep.tma_seg = -1;
+  for (int s = 0; s < ep.nseg; ++s) {
+    const EpiSeg& g = ep.seg[s];
+    if (g.kind == EPI_SOFTPLUS_Q) heavy = true;
+    if (g.kind == EPI_F32 && ep.tma_seg < 0 && (g.n0 % 32) == 0 && ((g.ld * 4) % 16) == 0 &&
+        ((uintptr_t)g.out % 16) == 0 && g.n1 - g.n0 >= 32)
+      ep.tma_seg = s;
+  }
+  if (heavy) return launch_tc<BN, 16, false>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+  if (ep.tma_seg >= 0) return launch_tc<BN, 8, true>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+  return launch_tc<BN, 8, false>(A, lda, Bt, ldb, M, N, Kp, ep, st);
 }
 
 cudaError_t measure_i8_peak(int iters, double* tops) {
@@ -399,14 +502,14 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
   if (path == 1 && !tc_ok) return cudaErrorInvalidValue;
   if (path == 1) {
     // Column tile: the largest BN that still gives >= 1 wave, else the smallest.
-    if (N <= 32) return launch_tc<32>(A, lda, Bt, ldb, M, N, Kp, ep, st);
-    if (N <= 64) return launch_tc<64>(A, lda, Bt, ldb, M, N, Kp, ep, st);
-    if (N <= 128) return launch_tc<128>(A, lda, Bt, ldb, M, N, Kp, ep, st);
-    if (N <= 192) return launch_tc<192>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (N <= 32) return launch_tc_bn<32>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (N <= 64) return launch_tc_bn<64>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (N <= 128) return launch_tc_bn<128>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (N <= 192) return launch_tc_bn<192>(A, lda, Bt, ldb, M, N, Kp, ep, st);
     const long long m_tiles = (M + TC_BM - 1) / TC_BM;
-    if (m_tiles * ((N + 255) / 256) >= num_sms()) return launch_tc<256>(A, lda, Bt, ldb, M, N, Kp, ep, st);
-    if (m_tiles * ((N + 127) / 128) >= num_sms()) return launch_tc<128>(A, lda, Bt, ldb, M, N, Kp, ep, st);
-    return launch_tc<64>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (m_tiles * ((N + 255) / 256) >= num_sms()) return launch_tc_bn<256>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (m_tiles * ((N + 127) / 128) >= num_sms()) return launch_tc_bn<128>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    return launch_tc_bn<64>(A, lda, Bt, ldb, M, N, Kp, ep, st);
   }
   const int vec = ((lda % 16) == 0 && (ldb % 16) == 0 && ((uintptr_t)A % 16) == 0 && ((uintptr_t)Bt % 16) == 0);
   constexpr int MB = 8;

@@ -56,6 +56,7 @@ struct EpiParams {
   int qmax;
   uint32_t* err;
   EpiSeg seg[3];
+  int tma_seg;  // index of an EPI_F32 segment written through a TMA store map (set by gemm_i8), or -1
 };
 
 __device__ __forceinline__ int find_seg(const EpiParams& ep, int n) {
