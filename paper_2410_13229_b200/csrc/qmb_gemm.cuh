@@ -40,13 +40,13 @@ __device__ __forceinline__ int qtab_count(const float* __restrict__ th, float v)
   int idx = 0;
 #pragma unroll
   for (int step = 64; step >= 1; step >>= 1)
-    if (v >= __ldg(th + idx + step - 1)) idx += step;
+    if (v >= th[idx + step - 1]) idx += step;  // th may live in shared or global memory
   return idx;
 }
 
 __device__ __forceinline__ int softplus_quant(float v, const float* __restrict__ qtab, float s_div, int qmax,
                                               uint32_t& err) {
-  if (qtab && fabsf(v) <= 3.402823466e38f && !(v >= __ldg(qtab + 128) && v <= __ldg(qtab + 129)))
+  if (qtab && fabsf(v) <= 3.402823466e38f && !(v >= qtab[128] && v <= qtab[129]))
     return qtab_count(qtab, v);
   return quant_i8(softplus_f32(v), s_div, qmax, err);
 }
