@@ -229,8 +229,8 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
               uint32_t w = 0;
 #pragma unroll
               for (int t = 0; t < 4; ++t) {
-                const int q = sg.kind == EPI_SOFTPLUS_Q ? softplus_quant(v[j + t], qtab, sg.out_div, ep.qmax, err)
-                                                        : quant_i8(v[j + t], sg.out_div, ep.qmax, err);
+                const int q = sg.kind == EPI_SOFTPLUS_Q ? softplus_quant(v[j + t], qtab, sg.out_div, sg.out_inv, ep.qmax, err)
+                                                        : quant_fast(v[j + t], sg.out_div, sg.out_inv, ep.qmax, err);
                 w |= ((uint32_t)(q & 0xff)) << (8 * t);
               }
               packed[j / 4] = w;
@@ -252,8 +252,8 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
                 static_cast<float*>(sj.out)[off] = v;
               else
                 static_cast<int8_t*>(sj.out)[off] =
-                    (int8_t)(sj.kind == EPI_SOFTPLUS_Q ? softplus_quant(v, qtab, sj.out_div, ep.qmax, err)
-                                                       : quant_i8(v, sj.out_div, ep.qmax, err));
+                    (int8_t)(sj.kind == EPI_SOFTPLUS_Q ? softplus_quant(v, qtab, sj.out_div, sj.out_inv, ep.qmax, err)
+                                                       : quant_fast(v, sj.out_div, sj.out_inv, ep.qmax, err));
             }
           }
         }
@@ -493,8 +493,10 @@ cudaError_t measure_i8_peak(int iters, double* tops) {
 }
 
 cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
-                    const EpiParams& ep, cudaStream_t st, int force_path) {
+                    const EpiParams& ep_in, cudaStream_t st, int force_path) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  EpiParams ep = ep_in;
+  for (int s = 0; s < ep.nseg; ++s) ep.seg[s].out_inv = 1.0f / ep.seg[s].out_div;  // RN f32 reciprocal
   const bool tc_ok = (lda % 16 == 0) && (ldb % 16 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)Bt % 16 == 0) &&
                      Kp > 0;
   int path = force_path;

@@ -27,6 +27,7 @@ struct EpiSeg {
   long long ld;         // output row stride (elements)
   const float* bias;    // per-column dequantized bias (indexed n - n0) or nullptr
   const float* qtab;    // EPI_SOFTPLUS_Q: verified threshold table (softplus_qtab) or nullptr
+  float out_inv;        // 1.0f / out_div (filled in by gemm_i8)
 };
 
 // Verified threshold table for a monotone-in-practice quantized function
@@ -44,10 +45,19 @@ __device__ __forceinline__ int qtab_count(const float* __restrict__ th, float v)
   return idx;
 }
 
-__device__ __forceinline__ int softplus_quant(float v, const float* __restrict__ qtab, float s_div, int qmax,
-                                              uint32_t& err) {
-  if (qtab && fabsf(v) <= 3.402823466e38f && !(v >= qtab[128] && v <= qtab[129]))
-    return qtab_count(qtab, v);
+// quantize(softplus(v)) through the verified table: start from a fast-math
+// estimate of the level and walk to the exact one, i.e. the count of
+// thresholds <= v (th ascending: th[k-1] <= v < th[k] <=> level k).
+__device__ __forceinline__ int softplus_quant(float v, const float* __restrict__ qtab, float s_div, float s_inv,
+                                              int qmax, uint32_t& err) {
+  if (qtab && fabsf(v) <= 3.402823466e38f && !(v >= qtab[128] && v <= qtab[129])) {
+    const float sp = v > 15.0f ? v : __logf(1.0f + __expf(v));
+    int q = __float2int_rn(fminf(sp * s_inv, 127.0f));
+    q = q < 0 ? 0 : q;
+    while (q > 0 && v < qtab[q - 1]) --q;
+    while (q < 127 && v >= qtab[q]) ++q;
+    return q;
+  }
   return quant_i8(softplus_f32(v), s_div, qmax, err);
 }
 
@@ -76,9 +86,9 @@ __device__ __forceinline__ void epi_store_one(const EpiParams& ep, const EpiSeg&
   if (sg.kind == EPI_F32) {
     static_cast<float*>(sg.out)[off] = v;
   } else if (sg.kind == EPI_SOFTPLUS_Q) {
-    static_cast<int8_t*>(sg.out)[off] = (int8_t)softplus_quant(v, sg.qtab, sg.out_div, ep.qmax, err);
+    static_cast<int8_t*>(sg.out)[off] = (int8_t)softplus_quant(v, sg.qtab, sg.out_div, sg.out_inv, ep.qmax, err);
   } else {
-    static_cast<int8_t*>(sg.out)[off] = (int8_t)quant_i8(v, sg.out_div, ep.qmax, err);
+    static_cast<int8_t*>(sg.out)[off] = (int8_t)quant_fast(v, sg.out_div, sg.out_inv, ep.qmax, err);
   }
 }
 

@@ -1,0 +1,79 @@
+#!/usr/bin/env python
+"""One Mamba-2.8B-shape W8A8 layer (synthetic weights, GPU-calibrated scales)
+prefilled at B x T tokens between cudaProfilerStart/Stop, for
+`ncu --profile-from-start off`.  Also prints per-stage CUDA-event times."""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import dataclasses
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="2.8b")
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--seq", type=int, default=1024)
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    import torch
+
+    from paper_2410_13229_b200 import _device, _lib
+    from paper_2410_13229_b200.model import device_model
+    from paper_2410_13229_b200.synthetic import CONFIGS, build_model
+
+    cfg = dataclasses.replace(CONFIGS[args.config], n_layers=1, vocab_size=1024)
+    qm = build_model(cfg, seed=0, calib_tokens=128)
+    dm = device_model(qm)
+    dev = _device.device()
+    B, T = args.batch, args.seq
+    tokens = torch.randint(0, cfg.vocab_size, (B, T), device=dev)
+    for _ in range(2):
+        dm.forward_hidden(tokens)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    dm.forward_hidden(tokens)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    _device.err_flag().raise_if_set()
+    # per-stage event timing (outside the profiled range)
+    lib = _lib.load()
+    blk = dm.blocks[0]
+    M = B * T
+    u = torch.randint(-127, 128, (M, cfg.d_model), dtype=torch.int8, device=dev)
+    out = torch.empty((M, cfg.d_model), dtype=torch.float32, device=dev)
+    ws = _device.workspace(blk.workspace_bytes(M))
+    ms = (ctypes.c_float * 7)()
+    acc = [0.0] * 7
+    for r in range(args.reps + 1):
+        _lib.check(lib.qmb_block_prefill_profiled(blk.handle, u.data_ptr(), 0.0, B, T, out.data_ptr(), 0,
+                                                  ws.data_ptr(), ws.numel(), _device.err_flag().ptr,
+                                                  torch.cuda.current_stream().cuda_stream, ms))
+        if r:
+            acc = [a + m / args.reps for a, m in zip(acc, ms)]
+    names = ["in_proj", "conv", "x_proj", "dt_proj", "scan", "hadamard_quant", "out_proj"]
+    x_out = torch.randn((M, cfg.d_model), device=dev)
+    x_res = torch.randn((M, cfg.d_model), device=dev)
+    u_q = torch.empty((M, cfg.d_model), dtype=torch.int8, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dm._rmsnorm(x_out, x_res, x_res, dm.norms[0], dm.s_in[0], u_q, None, M, _device.err_flag(),
+                torch.cuda.current_stream().cuda_stream)
+    e0.record()
+    for _ in range(args.reps):
+        dm._rmsnorm(x_out, x_res, x_res, dm.norms[0], dm.s_in[0], u_q, None, M, _device.err_flag(),
+                    torch.cuda.current_stream().cuda_stream)
+    e1.record()
+    torch.cuda.synchronize()
+    res = dict(zip(names, [round(a, 4) for a in acc]))
+    res["rmsnorm"] = round(e0.elapsed_time(e1) / args.reps, 4)
+    res["total_layer_ms"] = round(sum(res.values()), 4)
+    print(json.dumps({"stage_ms": res, "M": M}))
+
+
+if __name__ == "__main__":
+    main()
