@@ -196,6 +196,11 @@ int qmb_eval_math(int fn, const float* x, float* y, long long n, qmb_stream_t st
  * 128x256x32 MMAs on every SM (roofline denominator; synchronizes). */
 int qmb_measure_i8_peak(int iters, double* tops);
 
+/* GEMM tuning probe on synthetic operands: average ms of the tcgen05 GEMM at
+ * M x N x K with epilogue `mode` (0 f32/TMA store, 1 int8, 2 f32 direct,
+ * 3 int8|f32 split as in_proj, 4 softplus+quant). Allocates; synchronizes. */
+int qmb_gemm_bench(int M, int N, int K, int mode, int iters, float* ms);
+
 /* Embedding row gather (model.py:249): out[r] = table[tokens[r]]. */
 int qmb_embed_gather(const float* table, const long long* tokens, long long n, int D, float* out,
                      qmb_stream_t stream);

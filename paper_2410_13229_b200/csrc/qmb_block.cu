@@ -725,6 +725,12 @@ extern "C" int qmb_hadamard_quantize(const float* y, long long M, int p, int m, 
   return 0;
 }
 
+extern "C" int qmb_gemm_bench(int M, int N, int K, int mode, int iters, float* ms) {
+  if (M <= 0 || N <= 0 || K <= 0 || K % 16 || iters <= 0 || !ms) return fail(QMB_E_ARG, "invalid argument");
+  QMB_CUDA(gemm_bench(M, N, K, mode, iters, ms), "gemm bench");
+  return 0;
+}
+
 extern "C" int qmb_measure_i8_peak(int iters, double* tops) {
   if (iters <= 0 || !tops) return fail(QMB_E_ARG, "invalid argument");
   QMB_CUDA(measure_i8_peak(iters, tops), "i8 peak probe");

@@ -48,6 +48,10 @@ __device__ __forceinline__ int qtab_count(const float* __restrict__ th, float v)
 // quantize(softplus(v)) through the verified table: start from a fast-math
 // estimate of the level and walk to the exact one, i.e. the count of
 // thresholds <= v (th ascending: th[k-1] <= v < th[k] <=> level k).
+static __device__ __noinline__ int softplus_quant_exact(float v, float s_div, int qmax, uint32_t* err) {
+  return quant_i8(softplus_f32(v), s_div, qmax, *err);
+}
+
 __device__ __forceinline__ int softplus_quant(float v, const float* __restrict__ qtab, float s_div, float s_inv,
                                               int qmax, uint32_t& err) {
   if (qtab && fabsf(v) <= 3.402823466e38f && !(v >= qtab[128] && v <= qtab[129])) {
@@ -58,7 +62,7 @@ __device__ __forceinline__ int softplus_quant(float v, const float* __restrict__
     while (q < 127 && v >= qtab[q]) ++q;
     return q;
   }
-  return quant_i8(softplus_f32(v), s_div, qmax, err);
+  return softplus_quant_exact(v, s_div, qmax, &err);
 }
 
 struct EpiParams {
@@ -66,7 +70,8 @@ struct EpiParams {
   int qmax;
   uint32_t* err;
   EpiSeg seg[3];
-  int tma_seg;  // index of an EPI_F32 segment written through a TMA store map (set by gemm_i8), or -1
+  int tma_seg;   // segments written through TMA store maps tmC / tmC2 (set by gemm_i8), or -1
+  int tma_seg2;
 };
 
 __device__ __forceinline__ int find_seg(const EpiParams& ep, int n) {
@@ -104,4 +109,5 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
 int num_sms();
 // Dense int8 tensor-core throughput (TOP/s) of back-to-back 128x256x32 UMMAs on all SMs.
 cudaError_t measure_i8_peak(int iters, double* tops);
+cudaError_t gemm_bench(int M, int N, int K, int mode, int iters, float* ms_out);
 }  // namespace qmb
