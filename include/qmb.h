@@ -100,6 +100,7 @@ enum {
   QMB_WS_DTR,      /* int8 [M, Rp]    x_proj -> dt_r */
   QMB_WS_DELTA,    /* int8 [M, E]     dt_proj+softplus -> delta_q */
   QMB_WS_YQ,       /* int8 [M, Ep]    Hadamard (or direct) quantized y */
+  QMB_WS_BCF,      /* f32  [M, 2N]    dequantized b | c rows (scan operand) */
   QMB_WS_COUNT
 };
 

@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
           continue;
         }
         if (m >= M) continue;
-        const long long ldb_bytes = sg.ld * (sg.kind == EPI_F32 ? 4 : 1);
+        const bool f32out = sg.kind == EPI_F32;
+        const long long ldb_bytes = sg.ld * (f32out ? 4 : 1);
         const bool fast = (nb + 32 <= sg.n1) && (nb + 32 <= N) && ((sg.n0 & 15) == 0) && (ldb_bytes % 16 == 0) &&
                           ((reinterpret_cast<uintptr_t>(sg.out) & 15) == 0);
         if (fast) {
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
               v[j + 3] = __fadd_rn(v[j + 3], bb.w);
             }
           }
-          if (sg.kind == EPI_F32) {
+          if (f32out) {
             float4* o = reinterpret_cast<float4*>(static_cast<float*>(sg.out) + m * sg.ld + (nb - sg.n0));
 #pragma unroll
             for (int j = 0; j < 32; j += 4) o[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);

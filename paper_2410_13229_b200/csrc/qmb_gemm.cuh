@@ -15,7 +15,7 @@ namespace qmb {
 enum EpiKind : int {
   EPI_QUANT = 0,     // int8 out = quantize(f32(acc) * s [+ bias])
   EPI_F32 = 1,       // f32 out = f32(acc) * s [+ bias]
-  EPI_SOFTPLUS_Q = 2 // int8 out = quantize(softplus(f32(acc) * s [+ bias]))
+  EPI_SOFTPLUS_Q = 2  // int8 out = quantize(softplus(f32(acc) * s [+ bias]))
 };
 
 struct EpiSeg {

@@ -76,12 +76,18 @@ struct ScanParams {
   const int8_t* dt; long long lddt;   // delta_q          [B*T, lddt]
   const int8_t* bq; const int8_t* cq; long long ldbc;  // [B*T, ldbc] each
   const float* z;   long long ldz;    // gate input z or nullptr (no gate)
+  int z_silu;                         // z already holds silu(z) (computed in the in_proj epilogue)
   float* y;         long long ldy;    // output (may alias z)
   const float* lut_x; const float* lut_dt; const float* lut_b; const float* lut_c;  // 256-entry, index q+128
   const float* a;                     // [E, N] dequantized a (direct-exp path)
   const uint8_t* a_col;               // [E, N] column into exp_lut (LUT path)
   const float* exp_lut; int exp_ncols;  // [128][exp_ncols]: expf(deq_dt[q] * a_col value), q in [0,127]
   const float* d;                     // [E] dequantized d
+  float* bcf;                         // [B*T, 2N] scratch for dequantized b | c rows (batch-tiled scan), or null
+  // {-0.0f, -0.0f} and {1.0f, 1.0f} as runtime operands: fma.rn.f32x2(a, b, NEGZ) is an
+  // exactly rounded product and fma.rn.f32x2(a, ONE, c) an exactly rounded sum; being
+  // opaque to ptxas they cannot be folded/contracted (literal constants would be).
+  unsigned long long negz2, one2;
   float* h;                           // [B, E, N] carried state (in if h_in, out if h_out)
   int h_in, h_out;
   int B, T, E, N;

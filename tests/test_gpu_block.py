@@ -95,6 +95,34 @@ def test_block_batched_sequences(cuda, oracle, name):
         assert np.array_equal(got[b], ref), b
 
 
+@pytest.mark.parametrize("name,B,T", [("m12_full", 20, 13), ("m20_full", 37, 9), ("s130m", 33, 17)])
+def test_block_many_sequences_bit_exact(cuda, oracle, name, B, T):
+    """Large batches take the batch-tiled scan (8 channels x 32 sequences per
+    CTA); ragged B / T / channel tails included.  Final states checked too."""
+    from paper_2410_13229_b200 import _device
+    from paper_2410_13229_b200.qblock import device_block
+
+    z, meta = load_block(name)
+    w = block_weights(z, meta)
+    qb = mirror_block(z, meta, w)
+    ob = oracle_block(z, meta, w)
+    dev = device_block(qb)
+    D, E, N = meta["cfg"]["d_model"], meta["cfg"]["d_inner"], meta["cfg"]["d_state"]
+    rng = np.random.default_rng(B * 100 + T)
+    u = rng.integers(-127, 128, size=(B, T, D)).astype(np.int8)
+    out = torch.empty((B * T, D), dtype=torch.float32, device="cuda")
+    conv, h = dev.new_state(B)
+    dev.prefill(torch.from_numpy(u).cuda().reshape(B * T, D), B, T, out, u_scale=meta["u_scale"],
+                conv_state_out=conv, ssm_state_out=h)
+    _device.err_flag().raise_if_set()
+    got = out.reshape(B, T, D).cpu().numpy()
+    hs = h.cpu().numpy()
+    for b in range(B):
+        st = oracle.block_stages(u[b], meta["u_scale"], ob)
+        assert np.array_equal(got[b].view(np.uint32), st["out"].view(np.uint32)), b
+        assert np.array_equal(hs[b].view(np.uint32), st["h"].view(np.uint32)), b
+
+
 @pytest.mark.parametrize("name", ["tiny_full", "m12_full", "p2_inper", "s2p8b"])
 def test_block_decode_equals_prefill(cuda, name):
     """Prefill k tokens (exporting state), then decode the rest one by one: every
