@@ -23,7 +23,7 @@ c_sz = ctypes.c_size_t
 QMB_ERR_NONFINITE = 1
 QMB_ERR_SCAN = 2
 QMB_NUM_ACT = 10
-WS_SLOTS = ("UPAD", "XQ", "Z", "SCANX", "B", "C", "DTR", "DELTA", "YQ", "BCF")
+WS_SLOTS = ("UPAD", "XQ", "Z", "SCANX", "B", "C", "DTR", "DELTA", "YQ", "BCF", "ACC32")
 
 
 class QWeight(ctypes.Structure):

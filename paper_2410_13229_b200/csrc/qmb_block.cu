@@ -285,6 +285,7 @@ static void ws_layout(const qmb_block* b, long long M, size_t off[QMB_WS_COUNT],
   off[QMB_WS_DELTA] = take((size_t)M * b->E);
   off[QMB_WS_YQ] = take((size_t)M * b->Ep);
   off[QMB_WS_BCF] = take((size_t)M * 2 * b->N * 4);
+  off[QMB_WS_ACC32] = take(M <= 128 ? (size_t)SPLITK_SCRATCH_INTS * 4 : 0);
   *total = o;
 }
 
@@ -332,6 +333,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
   int8_t* delta = (int8_t*)(w + off[QMB_WS_DELTA]);
   int8_t* yq = (int8_t*)(w + off[QMB_WS_YQ]);
   float* bcf = (float*)(w + off[QMB_WS_BCF]);
+  int32_t* acc32 = M <= 128 ? (int32_t*)(w + off[QMB_WS_ACC32]) : nullptr;
   const int D = b->D, E = b->E, N = b->N, R = b->R;
   const double s_u = u_scale > 0.0 ? u_scale : b->act[QMB_ACT_IN];
 
@@ -356,7 +358,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     // z-half stays raw f32: computing silu(z) in this epilogue made it outlast
     // the MMAs (measured 1.6 -> 5.6 ms per layer); the scan applies it.
     ep.seg[1] = EpiSeg{E, 2 * E, EPI_F32, s_lin, 1.0f, z, E, nullptr};
-    QMB_CUDA(gemm_i8(A, lda, b->w_in_t, b->Dp, (int)M, 2 * E, D, ep, st, 0), "in_proj gemm");
+    QMB_CUDA(gemm_i8(A, lda, b->w_in_t, b->Dp, (int)M, 2 * E, D, ep, st, 0, acc32), "in_proj gemm");
   }
   // conv + SiLU + requant (qblock.py:199-201 -> fused_qconv :126-143)
   const float s_conv = f32(b->act[QMB_ACT_CONV_IN] * b->s_conv_w);
@@ -396,7 +398,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     ep.seg[1] = EpiSeg{N, 2 * N, EPI_QUANT, f32(s_x * b->s_w_c * 1.0), f32(b->act[QMB_ACT_C]), cq, N, nullptr};
     ep.seg[2] = EpiSeg{2 * N, 2 * N + R, EPI_QUANT, f32(s_x * b->s_w_dtr * 1.0), f32(b->act[QMB_ACT_DT_R]), dtr,
                        b->Rp, nullptr};
-    QMB_CUDA(gemm_i8(scanx, b->Ep, b->w_x_t, b->Ep, (int)M, b->Nx, E, ep, st, 0), "x_proj gemm");
+    QMB_CUDA(gemm_i8(scanx, b->Ep, b->w_x_t, b->Ep, (int)M, b->Nx, E, ep, st, 0, acc32), "x_proj gemm");
   }
   // dt_proj + bias + softplus + quantize (qblock.py:205-206)
   PROF(3, st);
@@ -407,7 +409,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     ep.err = err;
     ep.seg[0] = EpiSeg{0, E, EPI_SOFTPLUS_Q, f32(b->act[QMB_ACT_DT_R] * b->s_w_dt * 1.0), f32(b->act[QMB_ACT_DT]),
                        delta, E, b->dt_bias, b->sp_qtab};
-    QMB_CUDA(gemm_i8(dtr, b->Rp, b->w_dt_t, b->Rp, (int)M, E, R, ep, st, 0), "dt_proj gemm");
+    QMB_CUDA(gemm_i8(dtr, b->Rp, b->w_dt_t, b->Rp, (int)M, E, R, ep, st, 0, acc32), "dt_proj gemm");
   }
   // scan + D skip + gate (qblock.py:207-210), gated y written over z
   PROF(4, st);
@@ -445,7 +447,9 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     sp.E = E;
     sp.N = N;
     sp.err = err;
-    const int use_lut = (scan_exp == 0 && !decode) ? 1 : 0;
+    // 1: tabulated expf in shared memory (prefill), 2: tabulated expf through L1
+    // (decode, one step per sequence), 0: direct FP64 glibc-expf restatement
+    const int use_lut = scan_exp != 0 ? 0 : (decode ? 2 : 1);
     QMB_CUDA(selective_scan(sp, use_lut, st), "scan");
   }
   // output quantization (qblock.py:211-214)
@@ -478,7 +482,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     const double s_y = b->had ? b->act[QMB_ACT_Y_HAD] : b->act[QMB_ACT_Y];
     const double extra = b->had ? 1.0 / (double)E : 1.0;
     ep.seg[0] = EpiSeg{0, D, EPI_F32, f32(s_y * b->s_w_out * extra), 1.0f, out, D, nullptr};
-    QMB_CUDA(gemm_i8(yq, b->Ep, b->w_out_t, b->Ep, (int)M, D, E, ep, st, 0), "out_proj gemm");
+    QMB_CUDA(gemm_i8(yq, b->Ep, b->w_out_t, b->Ep, (int)M, D, E, ep, st, 0, acc32), "out_proj gemm");
   }
   PROF(7, st);
   return 0;
@@ -512,7 +516,7 @@ extern "C" int qmb_block_decode(const qmb_block* b, const int8_t* u_q, double u_
                                 float* ssm_state, float* out, void* ws, size_t ws_bytes, uint32_t* err,
                                 qmb_stream_t stream) {
   if (!conv_state || !ssm_state) return fail(QMB_E_ARG, "decode requires conv and ssm state");
-  return block_run(b, u_q, u_scale, B, 1, out, conv_state, ssm_state, true, nullptr, nullptr, 1, ws, ws_bytes, err,
+  return block_run(b, u_q, u_scale, B, 1, out, conv_state, ssm_state, true, nullptr, nullptr, 0, ws, ws_bytes, err,
                    (cudaStream_t)stream);
 }
 

@@ -116,8 +116,18 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
 
   const int num_m = (M + TC_BM - 1) / TC_BM;
   const int num_n = (N + BN - 1) / BN;
-  const int num_tiles = num_m * num_n;
-  const int num_k = (Kp + TC_BK - 1) / TC_BK;
+  const int splitk = ep.splitk > 1 ? ep.splitk : 1;
+  const int num_tiles = num_m * num_n * splitk;
+  const int num_k_all = (Kp + TC_BK - 1) / TC_BK;
+  const int kper = (num_k_all + splitk - 1) / splitk;
+  // tile -> (m block, n block, K split): splits of one output tile are adjacent
+  auto tile_coords = [&](int tile, int& m0, int& n0, int& kb0, int& kb1) {
+    const int sk = tile % splitk, mn = tile / splitk;
+    m0 = (mn / num_n) * TC_BM;
+    n0 = (mn % num_n) * BN;
+    kb0 = sk * kper;
+    kb1 = min(num_k_all, kb0 + kper);
+  };
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
@@ -125,9 +135,9 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile / num_n) * TC_BM;
-        const int n0 = (tile % num_n) * BN;
-        for (int kb = 0; kb < num_k; ++kb) {
+        int m0, n0, kb0, kb1;
+        tile_coords(tile, m0, n0, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * TC_BK, m0);
@@ -152,14 +162,17 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
         mbar_wait(&tempty[buf], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tbase + (uint32_t)(buf * BN);
-        for (int kb = 0; kb < num_k; ++kb) {
+        int m0, n0, kb0, kb1;
+        tile_coords(tile, m0, n0, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < TC_BK / 32; ++k) {
-            umma_i8(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc, (kb | k) != 0);
+            umma_i8(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                    (kb > kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -186,8 +199,8 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int buf = it & 1;
       const uint32_t use = (uint32_t)(it >> 1);
-      const int m0 = (tile / num_n) * TC_BM;
-      const int n0 = (tile % num_n) * BN;
+      int m0, n0, kb0, kb1;
+      tile_coords(tile, m0, n0, kb0, kb1);
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const long long m = (long long)m0 + row;
@@ -198,6 +211,19 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
         tmem_ld_32x32b_x32(tcol + c * 32, r);
         const int nb = n0 + c * 32;
         if (nb >= N) continue;  // warp-uniform
+        if (splitk > 1) {       // split-K partial -> acc32[split][M][N]; summed (exactly) afterwards
+          if (m < M) {
+            int32_t* dst = ep.acc32 + ((long long)(tile % splitk) * M + m) * N + nb;
+            if (nb + 32 <= N && (N % 4) == 0) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<int4*>(dst + j) = make_int4((int)r[j], (int)r[j + 1], (int)r[j + 2], (int)r[j + 3]);
+            } else {
+              for (int j = 0; j < 32 && nb + j < N; ++j) dst[j] = (int)r[j];
+            }
+          }
+          continue;
+        }
         const int s = find_seg(ep, nb);
         const EpiSeg& sg = ep.seg[s];
         const int slot = TMAOUT ? (s == ep.tma_seg ? 0 : (s == ep.tma_seg2 ? 1 : -1)) : -1;
@@ -507,7 +533,7 @@ static cudaError_t launch_tc(const int8_t* A, long long lda, const int8_t* Bt, l
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN) * (ep.splitk > 1 ? ep.splitk : 1);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   gemm_i8_tc_kernel<BN, EPIW, TMAOUT><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(tmA, tmB, tmC, tmC2, M, N, Kp, ep);
   return cudaGetLastError();
@@ -620,26 +646,77 @@ cudaError_t gemm_bench(int M, int N, int K, int mode, int iters, float* ms_out) 
   return e;
 }
 
+// Epilogue of a split-K GEMM: the exact int32 sums in acc32 [M, N] through the
+// same per-element float steps as the fused epilogue.
+__global__ void epi_apply_kernel(const int32_t* __restrict__ acc, int splitk, int M, int N, EpiParams ep) {
+  uint32_t err = 0;
+  const long long total = (long long)M * N;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long m = k / N;
+    const int n = (int)(k - m * N);
+    int s = 0;
+    for (int sk = 0; sk < splitk; ++sk) s += acc[sk * total + k];  // int32: exact in any order
+    epi_store_one(ep, ep.seg[find_seg(ep, n)], m, n, s, err);
+  }
+  flag_error(ep.err, err);
+}
+
+template <int BN>
+static cudaError_t launch_tc_choose(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N,
+                                    int Kp, EpiParams ep, cudaStream_t st, int32_t* acc32) {
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
+  const int num_k = (Kp + TC_BK - 1) / TC_BK;
+  int splitk = 1;
+  if (acc32 && tiles * 2 <= num_sms() && num_k > 1) {
+    splitk = num_sms() / tiles;
+    if (splitk > num_k) splitk = num_k;
+    const int kper = (num_k + splitk - 1) / splitk;  // no empty splits
+    splitk = (num_k + kper - 1) / kper;
+  }
+  if (splitk <= 1) {
+    ep.splitk = 1;
+    return launch_tc_bn<BN>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+  }
+  EpiParams sp = ep;
+  sp.splitk = splitk;
+  sp.acc32 = acc32;
+  sp.tma_seg = sp.tma_seg2 = -1;
+  cudaError_t e = launch_tc<BN, 8, false>(A, lda, Bt, ldb, M, N, Kp, sp, st);
+  if (e != cudaSuccess) return e;
+  ep.splitk = 1;
+  const long long total = (long long)M * N;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  epi_apply_kernel<<<(unsigned)blocks, 256, 0, st>>>(acc32, splitk, M, N, ep);
+  return cudaGetLastError();
+}
+
 cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
-                    const EpiParams& ep_in, cudaStream_t st, int force_path) {
+                    const EpiParams& ep_in, cudaStream_t st, int force_path, int32_t* acc32) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   EpiParams ep = ep_in;
+  ep.splitk = 1;
+  ep.acc32 = nullptr;
   for (int s = 0; s < ep.nseg; ++s) ep.seg[s].out_inv = 1.0f / ep.seg[s].out_div;  // RN f32 reciprocal
   const bool tc_ok = (lda % 16 == 0) && (ldb % 16 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)Bt % 16 == 0) &&
                      Kp > 0;
   int path = force_path;
-  if (path == 0) path = (tc_ok && M > 16) ? 1 : 2;
+  if (path == 0) path = (tc_ok && (M > 16 || acc32)) ? 1 : 2;
   if (path == 1 && !tc_ok) return cudaErrorInvalidValue;
   if (path == 1) {
+    if (M > TC_BM) acc32 = nullptr;  // split-K only for skinny (decode-like) M
     // Column tile: the largest BN that still gives >= 1 wave, else the smallest.
-    if (N <= 32) return launch_tc_bn<32>(A, lda, Bt, ldb, M, N, Kp, ep, st);
-    if (N <= 64) return launch_tc_bn<64>(A, lda, Bt, ldb, M, N, Kp, ep, st);
-    if (N <= 128) return launch_tc_bn<128>(A, lda, Bt, ldb, M, N, Kp, ep, st);
-    if (N <= 192) return launch_tc_bn<192>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (N <= 32) return launch_tc_choose<32>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
+    if (N <= 64) return launch_tc_choose<64>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
+    if (N <= 128) return launch_tc_choose<128>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
+    if (N <= 192) return launch_tc_choose<192>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
     const long long m_tiles = (M + TC_BM - 1) / TC_BM;
-    if (m_tiles * ((N + 255) / 256) >= num_sms()) return launch_tc_bn<256>(A, lda, Bt, ldb, M, N, Kp, ep, st);
-    if (m_tiles * ((N + 127) / 128) >= num_sms()) return launch_tc_bn<128>(A, lda, Bt, ldb, M, N, Kp, ep, st);
-    return launch_tc_bn<64>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (m_tiles * ((N + 255) / 256) >= num_sms())
+      return launch_tc_choose<256>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
+    if (m_tiles * ((N + 127) / 128) >= num_sms())
+      return launch_tc_choose<128>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
+    return launch_tc_choose<64>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
   }
   const int vec = ((lda % 16) == 0 && (ldb % 16) == 0 && ((uintptr_t)A % 16) == 0 && ((uintptr_t)Bt % 16) == 0);
   constexpr int MB = 8;

@@ -72,6 +72,8 @@ struct EpiParams {
   EpiSeg seg[3];
   int tma_seg;   // segments written through TMA store maps tmC / tmC2 (set by gemm_i8), or -1
   int tma_seg2;
+  int splitk;      // > 1: split-K over K blocks; partial int32 sums stored per split
+  int32_t* acc32;  // [splitk, M, N] int32 partials; a second kernel sums them and runs the epilogue
 };
 
 __device__ __forceinline__ int find_seg(const EpiParams& ep, int n) {
@@ -104,8 +106,13 @@ namespace qmb {
 // A: [M, Kp] with row stride lda bytes; Bt: [N, Kp] with row stride ldb bytes.
 // Requirements for the tensor-core path: lda % 16 == 0, ldb % 16 == 0, 16-byte
 // aligned base pointers.  Rows beyond M / N and K beyond Kp are zero-filled by TMA.
+// acc32_scratch (nullable): int32 scratch of >= SPLITK_SCRATCH_INTS enabling
+// split-K for skinny M (decode), where too few output tiles exist to keep the
+// SMs streaming weights.
+constexpr long long SPLITK_SCRATCH_INTS = 148LL * 128 * 256;
 cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
-                    const EpiParams& ep, cudaStream_t st, int force_path /*0 auto, 1 tc, 2 simt*/);
+                    const EpiParams& ep, cudaStream_t st, int force_path /*0 auto, 1 tc, 2 simt*/,
+                    int32_t* acc32_scratch = nullptr);
 int num_sms();
 // Dense int8 tensor-core throughput (TOP/s) of back-to-back 128x256x32 UMMAs on all SMs.
 cudaError_t measure_i8_peak(int iters, double* tops);

@@ -1,8 +1,24 @@
 // qmb_kernels.cuh -- launch interfaces of the non-GEMM kernels.
 #pragma once
+#include <mutex>
+#include <unordered_map>
+
 #include "qmb_common.cuh"
 
 namespace qmb {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size, so
+// that launches stay legal (and cheap) inside CUDA-graph stream capture.
+inline cudaError_t ensure_smem_attr(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find(fn);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done[fn] = bytes;
+  return e;
+}
 
 // ---------------------------------------------------------------- RMSNorm
 // numpy pairwise-sum plan for a row of length n (loops_utils.h.src pairwise_sum):
@@ -93,6 +109,8 @@ struct ScanParams {
   int B, T, E, N;
   uint32_t* err;
 };
+// use_lut: 1 = per-layer expf table in shared memory (prefill kernels), 2 = same
+// table read through L1 (decode), 0 = direct FP64 glibc-expf restatement.
 cudaError_t selective_scan(const ScanParams& p, int use_lut, cudaStream_t st);
 // exp_lut[r * ncols + c] = glibc_expf(lut_dt[r + 128] * a_vals[c]) for r in [0, 127]
 cudaError_t build_exp_lut(const float* lut_dt, const float* a_vals, int ncols, float* exp_lut, cudaStream_t st);

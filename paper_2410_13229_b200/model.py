@@ -179,17 +179,50 @@ class DeviceModel:
         ws = torch.empty(max(b.workspace_bytes(B) for b in self.blocks), dtype=torch.uint8, device=dev)
         return x_out, x_res, u_q, final, ws
 
-    def greedy_generate(self, prompt: torch.Tensor, steps: int) -> torch.Tensor:
+    def capture_decode(self, states):
+        """Capture one decode step over all layers (embed, 64 x (norm + 7 block
+        kernels), final norm, LM head) into a CUDA graph bound to `states`.
+        Returns (graph, token_in [B] int64, logits_out [B, V]); replay after
+        writing the next tokens into token_in."""
+        B = states[0][1].shape[0]
+        dev = _device.device()
+        bufs = self.decode_buffers(B)
+        tok = torch.zeros(B, dtype=torch.int64, device=dev)
+        scratch = self.new_states(B)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # lazy init (kernel attributes, cuBLAS) outside the capture
+            self.decode_step(tok, scratch, bufs=bufs)
+            self.decode_step(tok, scratch, bufs=bufs)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        _device.err_flag().reset()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            logits = self.decode_step(tok, states, bufs=bufs)
+        graph._qmb_keep = (bufs, scratch)  # keep captured buffers alive with the graph
+        return graph, tok, logits
+
+    def greedy_generate(self, prompt: torch.Tensor, steps: int, use_graph: bool = True) -> torch.Tensor:
         """Greedy decoding with carried state (quantized analogue of
-        model.greedy_decode, model.py:364-379).  prompt [B, T] -> [B, T+steps]."""
+        model.greedy_decode, model.py:364-379).  prompt [B, T] -> [B, T+steps].
+        Decode steps replay one captured CUDA graph."""
         logits, states = self.prefill(prompt)
         out = [prompt]
-        bufs = self.decode_buffers(prompt.shape[0])
+        if use_graph and steps > 1:
+            graph, tok, glogits = self.capture_decode(states)
+        else:
+            bufs = self.decode_buffers(prompt.shape[0])
         for s in range(steps):
             nxt = torch.argmax(logits, dim=-1)
             out.append(nxt[:, None])
             if s + 1 < steps:
-                logits = self.decode_step(nxt, states, bufs=bufs)
+                if use_graph and steps > 1:
+                    tok.copy_(nxt)
+                    graph.replay()
+                    logits = glogits
+                else:
+                    logits = self.decode_step(nxt, states, bufs=bufs)
         _device.err_flag().raise_if_set()
         return torch.cat(out, dim=1)
 
