@@ -54,7 +54,7 @@ __device__ __noinline__ void epi_chunk_scalar(const EpiParams& ep, const uint32_
   for (int j = 0; j < 32; ++j) {
     const int n = nb + j;
     if (n >= N) break;
-    const EpiSeg& sj = ep.seg[find_seg(ep, n)];
+    const EpiSeg sj = pick_seg(ep, find_seg(ep, n));
     float v = __fmul_rn(__int2float_rn((int)r[j]), sj.acc_scale);
     if (sj.bias) v = __fadd_rn(v, sj.bias[n - sj.n0]);
     const long long off = m * sj.ld + (n - sj.n0);
@@ -69,7 +69,7 @@ template <int BN, int EPIW, bool TMAOUT>
 __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
     gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2, int M,
-                      int N, int Kp, EpiParams ep) {
+                      int N, int Kp, const __grid_constant__ EpiParams ep) {
   using C = TcCfg<BN, EPIW, TMAOUT>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
           continue;
         }
         const int s = find_seg(ep, nb);
-        const EpiSeg& sg = ep.seg[s];
+        const EpiSeg sg = pick_seg(ep, s);
         const int slot = TMAOUT ? (s == ep.tma_seg ? 0 : (s == ep.tma_seg2 ? 1 : -1)) : -1;
         if (TMAOUT && slot >= 0 && nb + 32 <= sg.n1 && nb + 32 <= N) {
           // 32 rows x 32 cols through swizzled smem -> TMA store (rows >= M are clipped by TMA)
@@ -335,7 +335,10 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
             o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
           }
         } else {
-          epi_chunk_scalar<EPIW == 16>(ep, r, nb, N, m, qtab, err);
+          uint32_t rr[32];  // copy: passing r itself by reference would pin it to local memory
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rr[j] = r[j];
+          epi_chunk_scalar<EPIW == 16>(ep, rr, nb, N, m, qtab, err);
         }
       }
       tc_fence_before();
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(256) gemm_i8_simt_kernel(const int8_t* __restr
     for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
   }
   uint32_t err = 0;
-  const EpiSeg& sg = ep.seg[find_seg(ep, n)];
+  const EpiSeg sg = pick_seg(ep, find_seg(ep, n));
 #pragma unroll
   for (int i = 0; i < MB; ++i) {
     if (lane == i && m0 + i < M) epi_store_one(ep, sg, m0 + i, n, acc[i], err);
@@ -657,7 +660,7 @@ __global__ void epi_apply_kernel(const int32_t* __restrict__ acc, int splitk, in
     const int n = (int)(k - m * N);
     int s = 0;
     for (int sk = 0; sk < splitk; ++sk) s += acc[sk * total + k];  // int32: exact in any order
-    epi_store_one(ep, ep.seg[find_seg(ep, n)], m, n, s, err);
+    epi_store_one(ep, pick_seg(ep, find_seg(ep, n)), m, n, s, err);
   }
   flag_error(ep.err, err);
 }

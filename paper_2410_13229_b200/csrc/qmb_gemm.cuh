@@ -52,16 +52,22 @@ static __device__ __noinline__ int softplus_quant_exact(float v, float s_div, in
   return quant_i8(softplus_f32(v), s_div, qmax, *err);
 }
 
+// Branch-free level: fast-math estimate q0, then a +/-1 correction from the two
+// neighbouring thresholds.  The exhaustive sweep at handle creation verifies
+// THIS function against the exact one for all 2^32 inputs (qmb_kernels.cu);
+// inputs in the recorded disagreement hull take the exact path.
+__device__ __forceinline__ int softplus_quant_table(float v, const float* __restrict__ th, float s_inv) {
+  const float sp = v > 15.0f ? v : __logf(1.0f + __expf(v));
+  int q0 = __float2int_rn(fminf(fmaxf(sp * s_inv, 0.0f), 127.0f));
+  const float up = th[q0];                      // th[127] = +inf
+  const float dn = q0 > 0 ? th[q0 - 1] : -3.402823466e38f;
+  return q0 + (v >= up ? 1 : 0) - (v < dn ? 1 : 0);
+}
+
 __device__ __forceinline__ int softplus_quant(float v, const float* __restrict__ qtab, float s_div, float s_inv,
                                               int qmax, uint32_t& err) {
-  if (qtab && fabsf(v) <= 3.402823466e38f && !(v >= qtab[128] && v <= qtab[129])) {
-    const float sp = v > 15.0f ? v : __logf(1.0f + __expf(v));
-    int q = __float2int_rn(fminf(sp * s_inv, 127.0f));
-    q = q < 0 ? 0 : q;
-    while (q > 0 && v < qtab[q - 1]) --q;
-    while (q < 127 && v >= qtab[q]) ++q;
-    return q;
-  }
+  if (qtab && fabsf(v) <= 3.402823466e38f && !(v >= qtab[128] && v <= qtab[129]))
+    return softplus_quant_table(v, qtab, s_inv);
   return softplus_quant_exact(v, s_div, qmax, &err);
 }
 
@@ -75,6 +81,12 @@ struct EpiParams {
   int splitk;      // > 1: split-K over K blocks; partial int32 sums stored per split
   int32_t* acc32;  // [splitk, M, N] int32 partials; a second kernel sums them and runs the epilogue
 };
+
+// Segment by value with compile-time indices only: a runtime index into the
+// param-space array would make the compiler copy it to local memory.
+__device__ __forceinline__ EpiSeg pick_seg(const EpiParams& ep, int s) {
+  return s == 0 ? ep.seg[0] : (s == 1 ? ep.seg[1] : ep.seg[2]);
+}
 
 __device__ __forceinline__ int find_seg(const EpiParams& ep, int n) {
   int s = 0;
