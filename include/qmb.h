@@ -191,8 +191,15 @@ int qmb_hadamard_quantize(const float* y, long long M, int p, int m, const int8_
                           uint32_t* err_flag, qmb_stream_t stream);
 
 /* Elementwise restated transcendentals (parity harness): fn 0 np.exp f32,
- * 1 glibc expf, 2 glibc log1pf, 3 softplus (np.logaddexp(x,0)), 4 silu. */
+ * 1 glibc expf, 2 glibc log1pf, 3 softplus (np.logaddexp(x,0)), 4 silu,
+ * 5 silu hot-path variant (must equal 4 everywhere). */
 int qmb_eval_math(int fn, const float* x, float* y, long long n, qmb_stream_t stream);
+
+/* Exhaustive check: fn_a and fn_b bit-identical on all 2^32 float inputs?
+ * Device outputs: *mismatches (count), *first_bad (smallest mismatching bit
+ * pattern, 0xffffffff if none). */
+int qmb_verify_math(int fn_a, int fn_b, unsigned long long* mismatches, uint32_t* first_bad,
+                    qmb_stream_t stream);
 
 /* Measured dense int8 tensor-core peak (TOP/s): back-to-back tcgen05 kind::i8
  * 128x256x32 MMAs on every SM (roofline denominator; synchronizes). */

@@ -69,6 +69,7 @@ PROTOTYPES = {
     "qmb_measure_i8_peak": (c_int, [c_int, ctypes.POINTER(c_dbl)]),
     "qmb_gemm_bench": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(ctypes.c_float)]),
     "qmb_eval_math":(c_int, [c_int, c_vp, c_vp, c_ll, c_vp]),
+    "qmb_verify_math":(c_int, [c_int, c_int, c_vp, c_vp, c_vp]),
     "qmb_embed_gather": (c_int, [c_vp, c_vp, c_ll, c_int, c_vp, c_vp]),
 }
 

@@ -8,6 +8,8 @@
 // steps in the reference's order (int32 -> f32 RN, * f32 scale, + f32 bias,
 // optional softplus, quantize).
 #pragma once
+#include <cuda.h>
+
 #include "qmb_common.cuh"
 
 namespace qmb {
@@ -126,6 +128,10 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
                     const EpiParams& ep, cudaStream_t st, int force_path /*0 auto, 1 tc, 2 simt*/,
                     int32_t* acc32_scratch = nullptr);
 int num_sms();
+// Tiled TMA map of a rank-3 tensor: dims innermost first, byte strides of dims 1, 2;
+// elem 1 = uint8, 4 = float32; swizzle 0 / 64 / 128 (bytes).
+bool make_tmap_3d(CUtensorMap* tm, int elem, const void* base, const long long dims[3],
+                  const long long strides[2], const int box[3], int swizzle);
 // Dense int8 tensor-core throughput (TOP/s) of back-to-back 128x256x32 UMMAs on all SMs.
 cudaError_t measure_i8_peak(int iters, double* tops);
 cudaError_t gemm_bench(int M, int N, int K, int mode, int iters, float* ms_out);

@@ -126,5 +126,8 @@ cudaError_t embed_gather(const float* table, const long long* tokens, long long 
                          cudaStream_t st);
 // Elementwise exact transcendentals (for the parity harness).
 cudaError_t eval_math(int fn, const float* x, float* y, long long n, cudaStream_t st);
+// Bitwise comparison of eval_math functions fa, fb over all 2^32 float inputs
+// (device counters: mismatch count, smallest mismatching bit pattern or ~0u).
+cudaError_t verify_math(int fa, int fb, unsigned long long* bad, uint32_t* first, cudaStream_t st);
 
 }  // namespace qmb

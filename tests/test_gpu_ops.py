@@ -34,6 +34,20 @@ def test_transcendentals_bit_exact(cuda, oracle, fn, name):
     assert same.all(), f"{name}: {np.count_nonzero(~same)} mismatches, e.g. x={x[~same][:5]}"
 
 
+@pytest.mark.parametrize("fa,fb", [(4, 5)])
+def test_hot_path_math_exhaustive(cuda, fa, fb):
+    """Hot-path restatements equal the reference restatement on ALL 2^32 inputs."""
+    from paper_2410_13229_b200 import _device, _lib
+
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    first = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("qmb_verify_math", fa, fb, bad.data_ptr(), first.data_ptr(), _device.stream_ptr())
+    torch.cuda.synchronize()
+    n, f = int(bad.item()), int(first.item()) & 0xFFFFFFFF
+    x = np.array([f], np.uint32).view(np.float32)[0]
+    assert n == 0, f"{n} mismatches, first at bits {f:#010x} (x={x!r})"
+
+
 def test_quantize_known_answers(cuda):
     from paper_2410_13229_b200 import quantize
 

@@ -15,6 +15,6 @@ for SPEC in $SPECS; do
   ncu -i "$REP.ncu-rep" --page source --csv --print-source sass > "$REP.source.csv" 2>/dev/null
   gzip -f "$REP.source.csv"
   SZ=$(stat -c %s "$REP.ncu-rep" 2>/dev/null || echo 0)
-  if [ "$SZ" -gt 12000000 ]; then rm -f "$REP.ncu-rep"; fi
+  if [ "$SZ" -gt 3000000 ]; then rm -f "$REP.ncu-rep"; fi
 done
 ls -la "$OUT"
