@@ -32,7 +32,7 @@ struct TcCfg {
   static constexpr int TMEM_COLS =
       (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int SMEM_BYTES =
-      1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + QTAB_FLOATS * 4 + (2 * STAGES + 4) * 8 + 16;
+      1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + ((QTAB_FLOATS + 1) & ~1) * 4 + (2 * STAGES + 4) * 8 + 16;
   static_assert(STAGES >= 2, "pipeline too shallow");
 };
 
@@ -43,6 +43,60 @@ __device__ __forceinline__ int epi_quant(float v, const EpiSeg& g, const float* 
     if (g.kind == EPI_SOFTPLUS_Q) return softplus_quant(v, qtab, g.out_div, g.out_inv, qmax, err);
   }
   return quant_fast(v, g.out_div, g.out_inv, qmax, err);
+}
+
+// Rare fix-up of a softplus chunk: redo the elements outside the table's
+// verified domain with the exact formula.
+static __device__ __noinline__ void epi_softplus_fix(const float (&v)[32], const EpiSeg& g, const float* qtab,
+                                                     int qmax, uint32_t& err, uint32_t (&packed)[8]) {
+  const float lo = qtab[QTAB_LO], hi = qtab[QTAB_HI];
+#pragma unroll 1
+  for (int j = 0; j < 32; ++j) {
+    if (!softplus_table_miss(v[j], lo, hi)) continue;
+    const int q = softplus_quant_exact(v[j], g.out_div, qmax, &err);
+    const int sh = 8 * (j & 3);
+    packed[j >> 2] = (packed[j >> 2] & ~(0xffu << sh)) | ((uint32_t)(q & 0xff) << sh);
+  }
+}
+
+// 32 epilogue values -> 32 int8 (packed little-endian)
+template <bool SP>
+__device__ __forceinline__ void epi_quant32(const float (&v)[32], const EpiSeg& g, const float* qtab, int qmax,
+                                            uint32_t& err, uint32_t (&packed)[8]) {
+  if constexpr (SP) {
+    if (g.kind == EPI_SOFTPLUS_Q && qtab) {
+      const float lo = qtab[QTAB_LO], hi = qtab[QTAB_HI], qmaxf = (float)qmax;
+      float chk = 0.0f;  // NaN-sticky: becomes NaN iff some v is not finite
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int q = softplus_quant_table(v[j + t], qtab, g.out_inv, qmaxf);
+          chk = __fmaf_rn(v[j + t], 0.0f, chk);
+          w |= ((uint32_t)(q & 0xff)) << (8 * t);
+        }
+        packed[j / 4] = w;
+      }
+      bool miss = !(chk == 0.0f);
+      if (lo <= hi) {  // a disagreement interval exists (uniform; typically empty)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) miss |= (v[j] >= lo && v[j] <= hi);
+      }
+      if (miss) epi_softplus_fix(v, g, qtab, qmax, err, packed);
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 32; j += 4) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int q = epi_quant<SP>(v[j + t], g, qtab, qmax, err);
+      w |= ((uint32_t)(q & 0xff)) << (8 * t);
+    }
+    packed[j / 4] = w;
+  }
 }
 
 // Ragged / misaligned chunk (segment boundary inside the chunk, tails, odd
@@ -73,12 +127,13 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
   using C = TcCfg<BN, EPIW, TMAOUT>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by offsetting the shared array itself (keeps LDS/STS addressing)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
   uint8_t* sStg = smem + STAGES * C::STAGE_BYTES;  // 1024-aligned
   float* sQtab = reinterpret_cast<float*>(sStg + C::STG_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sQtab + QTAB_FLOATS + 2);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sQtab + ((QTAB_FLOATS + 1) & ~1));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -138,7 +193,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
         int m0, n0, kb0, kb1;
         tile_coords(tile, m0, n0, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_sleep(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * TC_BK, m0);
           tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * TC_BK, n0);
@@ -159,13 +214,13 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
         const int buf = it & 1;
         const uint32_t use = (uint32_t)(it >> 1);
-        mbar_wait(&tempty[buf], (use & 1) ^ 1);
+        mbar_wait_sleep(&tempty[buf], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tbase + (uint32_t)(buf * BN);
         int m0, n0, kb0, kb1;
         tile_coords(tile, m0, n0, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait_sleep(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
@@ -201,7 +256,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
       const uint32_t use = (uint32_t)(it >> 1);
       int m0, n0, kb0, kb1;
       tile_coords(tile, m0, n0, kb0, kb1);
-      mbar_wait(&tfull[buf], use & 1);
+      mbar_wait_sleep(&tfull[buf], use & 1);
       tc_fence_after();
       const long long m = (long long)m0 + row;
       const uint32_t tcol = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN);
@@ -266,16 +321,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
             }
           } else {
             uint32_t packed[8];
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              uint32_t w = 0;
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                const int q = epi_quant<EPIW == 16>(v[j + t], sg, qtab, ep.qmax, err);
-                w |= ((uint32_t)(q & 0xff)) << (8 * t);
-              }
-              packed[j / 4] = w;
-            }
+            epi_quant32<EPIW == 16>(v, sg, qtab, ep.qmax, err, packed);
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
             // 32 rows x 32 B, SWIZZLE_32B: 16B chunk c of row r at chunk c ^ ((r >> 2) & 1)
@@ -320,16 +366,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
             for (int j = 0; j < 32; j += 4) o[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
           } else {
             uint32_t packed[8];
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              uint32_t w = 0;
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                const int q = epi_quant<EPIW == 16>(v[j + t], sg, qtab, ep.qmax, err);
-                w |= ((uint32_t)(q & 0xff)) << (8 * t);
-              }
-              packed[j / 4] = w;
-            }
+            epi_quant32<EPIW == 16>(v, sg, qtab, ep.qmax, err, packed);
             uint4* o = reinterpret_cast<uint4*>(static_cast<int8_t*>(sg.out) + m * sg.ld + (nb - sg.n0));
             o[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
             o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
@@ -418,7 +455,7 @@ __global__ void __launch_bounds__(256) gemm_i8_simt_kernel(const int8_t* __restr
 // used as the roofline denominator for the GEMMs.
 __global__ void __launch_bounds__(128, 1) umma_i8_peak_kernel(int iters, int* sink) {
   extern __shared__ uint8_t psm_raw[];
-  uint8_t* psm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(psm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* psm = psm_raw + ((1024u - (smem_u32(psm_raw) & 1023u)) & 1023u);
   __shared__ uint64_t done_bar;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5;
@@ -622,10 +659,11 @@ cudaError_t gemm_bench(int M, int N, int K, int mode, int iters, float* ms_out) 
   cudaMemset(A, 1, (size_t)M * K);
   cudaMemset(B, 1, (size_t)N * K);
   float h_tab[QTAB_FLOATS];
-  for (int k = 0; k < 127; ++k) h_tab[k] = logf(expm1f((k + 0.5f) * 0.01f));  // ~softplus^-1 level bounds
-  h_tab[127] = INFINITY;
+  h_tab[0] = -INFINITY;
+  for (int k = 1; k < 128; ++k) h_tab[k] = logf(expm1f((k - 0.5f) * 0.01f));  // ~softplus^-1 level bounds
   h_tab[128] = INFINITY;
-  h_tab[129] = -INFINITY;
+  h_tab[QTAB_LO] = INFINITY;
+  h_tab[QTAB_HI] = -INFINITY;
   cudaMemcpy(tab, h_tab, sizeof(h_tab), cudaMemcpyHostToDevice);
   EpiParams ep{};
   ep.qmax = 127;

@@ -32,44 +32,41 @@ struct EpiSeg {
   float out_inv;        // 1.0f / out_div (filled in by gemm_i8)
 };
 
-// Verified threshold table for a monotone-in-practice quantized function
-// q(v) = quantize(f(v)): th[k-1] = min{v : q(v) >= k} (k = 1..127, +inf pad),
-// th[128..129] = [lo, hi] interval of v where the table was found (by an
-// exhaustive sweep over all 2^32 floats at handle creation) to disagree with
-// the exact evaluation; there the exact formula is used.  Exact by construction.
-constexpr int QTAB_FLOATS = 130;
+// Verified threshold table for quantize(softplus(v)) (monotone non-decreasing):
+// tab[0] = -inf, tab[k] = min{v : q(v) >= k} for k = 1..127 (+inf past qmax),
+// tab[128] = +inf, and tab[QTAB_LO], tab[QTAB_HI] = the interval of v on which an
+// exhaustive sweep over all 2^32 floats at handle creation found the table
+// function below to disagree with the exact evaluation (empty: lo > hi); there,
+// and for non-finite v, the exact formula is used.  Exact by construction.
+constexpr int QTAB_FLOATS = 131;
+constexpr int QTAB_LO = 129, QTAB_HI = 130;
 
-__device__ __forceinline__ int qtab_count(const float* __restrict__ th, float v) {
-  int idx = 0;
-#pragma unroll
-  for (int step = 64; step >= 1; step >>= 1)
-    if (v >= th[idx + step - 1]) idx += step;  // th may live in shared or global memory
-  return idx;
+// The table function: a fast-math estimate q0 of the level, then a +/-1
+// correction from the two thresholds around it (level q <=> tab[q] <= v < tab[q+1]).
+// Branch-free; the sweep verifies exactly this function.
+__device__ __forceinline__ int softplus_quant_table(float v, const float* __restrict__ tab, float s_inv,
+                                                    float qmaxf) {
+  float e, l;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmul_rn(v, 1.44269504088896341f)));
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(__fadd_rn(1.0f, e)));
+  const float sp = v > 15.0f ? v : __fmul_rn(l, 0.693147180559945309f);
+  const int q0 = __float2int_rn(fminf(fmaxf(__fmul_rn(sp, s_inv), 0.0f), qmaxf));
+  return q0 + (v >= tab[q0 + 1] ? 1 : 0) - (v < tab[q0] ? 1 : 0);
 }
 
-// quantize(softplus(v)) through the verified table: start from a fast-math
-// estimate of the level and walk to the exact one, i.e. the count of
-// thresholds <= v (th ascending: th[k-1] <= v < th[k] <=> level k).
+// v needs the exact path (outside the verified domain of the table function)
+__device__ __forceinline__ bool softplus_table_miss(float v, float lo, float hi) {
+  return !(fabsf(v) <= 3.402823466e38f) || (v >= lo && v <= hi);
+}
+
 static __device__ __noinline__ int softplus_quant_exact(float v, float s_div, int qmax, uint32_t* err) {
   return quant_i8(softplus_f32(v), s_div, qmax, *err);
 }
 
-// Branch-free level: fast-math estimate q0, then a +/-1 correction from the two
-// neighbouring thresholds.  The exhaustive sweep at handle creation verifies
-// THIS function against the exact one for all 2^32 inputs (qmb_kernels.cu);
-// inputs in the recorded disagreement hull take the exact path.
-__device__ __forceinline__ int softplus_quant_table(float v, const float* __restrict__ th, float s_inv) {
-  const float sp = v > 15.0f ? v : __logf(1.0f + __expf(v));
-  int q0 = __float2int_rn(fminf(fmaxf(sp * s_inv, 0.0f), 127.0f));
-  const float up = th[q0];                      // th[127] = +inf
-  const float dn = q0 > 0 ? th[q0 - 1] : -3.402823466e38f;
-  return q0 + (v >= up ? 1 : 0) - (v < dn ? 1 : 0);
-}
-
 __device__ __forceinline__ int softplus_quant(float v, const float* __restrict__ qtab, float s_div, float s_inv,
                                               int qmax, uint32_t& err) {
-  if (qtab && fabsf(v) <= 3.402823466e38f && !(v >= qtab[128] && v <= qtab[129]))
-    return softplus_quant_table(v, qtab, s_inv);
+  if (qtab && !softplus_table_miss(v, qtab[QTAB_LO], qtab[QTAB_HI]))
+    return softplus_quant_table(v, qtab, s_inv, (float)qmax);
   return softplus_quant_exact(v, s_div, qmax, &err);
 }
 
