@@ -83,6 +83,8 @@ struct HadParams {
   float s_out;
   int qmax;
   uint32_t* err;
+  // set by hadamard_quant: packed {+-1, +-1} sign pairs (index 2*[lo < 0] + [hi < 0])
+  unsigned long long sgn2[4];
 };
 cudaError_t hadamard_quant(const HadParams& p, cudaStream_t st);
 
