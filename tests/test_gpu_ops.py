@@ -175,13 +175,26 @@ def test_hadamard_golden_and_quant(cuda, oracle):
     assert hadamard_quantize(np.array([[64.0, 0, 0, 0]], np.float32), 1.0, plan).values.tolist() == [[64] * 4]
 
 
-@pytest.mark.parametrize("M,D", [(3, 8), (6, 16), (33, 64), (50, 768), (17, 2560), (9, 1000)])
+@pytest.mark.parametrize("M,D", [(3, 8), (6, 16), (33, 64), (50, 768), (17, 2560), (9, 1000),
+                                 (700, 2560), (640, 768), (1200, 64), (600, 1000)])
 def test_rmsnorm_residual_quant_bit_exact(cuda, oracle, M, D):
+    """Small M: CTA-per-row kernel; M >= 592: warp-per-row kernels (balanced pairwise
+    tree for 2^k equal leaves, generic plan otherwise), incl. rows that take the
+    exact-division fallback (zeros, -0, tiny and huge magnitudes)."""
     from paper_2410_13229_b200 import fused_rmsnorm_quant
 
     rng = np.random.default_rng(M + D)
     x_out = (rng.standard_normal((M, D)) * 3).astype(np.float32)
     x_res = (rng.standard_normal((M, D)) * 2).astype(np.float32)
+    if M >= 600:
+        x_out[1, ::3] = 0.0
+        x_res[1, ::3] = -0.0
+        x_out[2] *= np.float32(1e-20)
+        x_res[2] *= np.float32(1e-20)
+        x_out[3, :5] = np.float32(3e-38)
+        x_res[3, :5] = 0.0
+        x_out[4] *= np.float32(1e15)
+        x_res[4] *= np.float32(1e15)
     gain = rng.uniform(0.5, 1.5, D).astype(np.float32)
     q, res = fused_rmsnorm_quant(x_out, x_res, gain, 0.02)
     rq, rres = oracle.fused_rmsnorm_quant(x_out, x_res, gain, 0.02)
