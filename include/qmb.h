@@ -100,7 +100,7 @@ enum {
   QMB_WS_DTR,      /* int8 [M, Rp]    x_proj -> dt_r */
   QMB_WS_DELTA,    /* int8 [M, E]     dt_proj+softplus -> delta_q */
   QMB_WS_YQ,       /* int8 [M, Ep]    Hadamard (or direct) quantized y */
-  QMB_WS_BCF,      /* f32  [M, 2N]    dequantized b | c rows (scan operand) */
+  QMB_WS_BCF,      /* f32  [M, 36]    dequantized b | c rows, 4 pad floats (scan operand, N = 16) */
   QMB_WS_ACC32,    /* int32 split-K partials (19 MB, only when M <= 128: decode) */
   QMB_WS_COUNT
 };

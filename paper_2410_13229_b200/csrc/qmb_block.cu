@@ -1,6 +1,7 @@
 // qmb_block.cu -- C-ABI entry points (include/qmb.h): the block handle
 // (quantize_block's product uploaded to HBM in kernel-native layouts) and the
 // prefill / decode orchestration of block_forward_q (qblock.py:185-215).
+#include <stdlib.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -46,6 +47,19 @@ inline int qmax_of(int bits) { return (1 << (bits - 1)) - 1; }
 // numpy semantics of the reference's scale constants
 inline float f32(double v) { return (float)v; }
 inline float deq(int q, double s) { return (float)((double)q * s); }
+// hi + lo split of a dequantization scale for the scan's ALU dequantization
+// fma(q, hi, q * lo); true iff it reproduces f32(f64(q) * s) for every int8 code
+// (checked here with the same IEEE single operations the device performs).
+inline bool deq_split(double s, float* hi, float* lo) {
+  *hi = (float)s;
+  *lo = (float)(s - (double)*hi);
+  for (int q = -128; q <= 127; ++q) {
+    volatile float prod = (float)q * *lo;
+    const float v = fmaf((float)q, *hi, prod);
+    if (v != deq(q, s)) return false;
+  }
+  return true;
+}
 
 }  // namespace
 
@@ -251,6 +265,8 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
   }
   e = build_exp_lut(b->luts + 256, avals_dev, b->exp_ncols, b->exp_lut, 0);
   if (e == cudaSuccess) e = build_softplus_qtab(f32(d->act[QMB_ACT_DT]), b->qmax, b->sp_qtab, scratch, 0);
+  // verified conv silu+quantize fast path for this layer's scale (cached)
+  if (e == cudaSuccess) (void)silu_quant_thr(f32(d->act[QMB_ACT_X]), b->qmax, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     cudaFree(b->mem);
@@ -284,7 +300,7 @@ static void ws_layout(const qmb_block* b, long long M, size_t off[QMB_WS_COUNT],
   off[QMB_WS_DTR] = take((size_t)M * b->Rp);
   off[QMB_WS_DELTA] = take((size_t)M * b->E);
   off[QMB_WS_YQ] = take((size_t)M * b->Ep);
-  off[QMB_WS_BCF] = take((size_t)M * 2 * b->N * 4);
+  off[QMB_WS_BCF] = take((size_t)M * 36 * 4);  // BCF_LD-float rows (scan staging pitch)
   off[QMB_WS_ACC32] = take(M <= 128 ? (size_t)SPLITK_SCRATCH_INTS * 4 : 0);
   *total = o;
 }
@@ -302,6 +318,16 @@ extern "C" int qmb_block_workspace_layout(const qmb_block* b, long long rows, si
   ws_layout(b, rows, offsets, &total);
   return 0;
 }
+// Where the gate's silu(z) is evaluated: the in_proj epilogue (default) or the
+// scan (QMB_ZSILU_IN_GEMM=0, kept for A/B measurements).  Same f32 values either way.
+static bool zsilu_in_gemm() {
+  static const bool v = [] {
+    const char* e = getenv("QMB_ZSILU_IN_GEMM");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 
 // ------------------------------------------------------------------ forward
 // Optional per-stage event recording (qmb_block_prefill_profiled).
@@ -355,9 +381,9 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     ep.err = err;
     const float s_lin = f32(s_u * b->s_w_in);
     ep.seg[0] = EpiSeg{0, E, EPI_QUANT, s_lin, f32(b->act[QMB_ACT_CONV_IN]), xq, E, nullptr};
-    // z-half stays raw f32: computing silu(z) in this epilogue made it outlast
-    // the MMAs (measured 1.6 -> 5.6 ms per layer); the scan applies it.
-    ep.seg[1] = EpiSeg{E, 2 * E, EPI_F32, s_lin, 1.0f, z, E, nullptr};
+    // z-half: silu(z) (the gate's factor, ssm.py:110-111) is computed here, in
+    // the epilogue that overlaps the MMAs, instead of in the issue-bound scan.
+    ep.seg[1] = EpiSeg{E, 2 * E, zsilu_in_gemm() ? EPI_F32_SILU : EPI_F32, s_lin, 1.0f, z, E, nullptr};
     QMB_CUDA(gemm_i8(A, lda, b->w_in_t, b->Dp, (int)M, 2 * E, D, ep, st, 0, acc32), "in_proj gemm");
   }
   // conv + SiLU + requant (qblock.py:199-201 -> fused_qconv :126-143)
@@ -424,7 +450,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     sp.ldbc = N;
     sp.z = z;
     sp.ldz = E;
-    sp.z_silu = 0;
+    sp.z_silu = zsilu_in_gemm() ? 1 : 0;
     sp.y = z;
     sp.ldy = E;
     sp.lut_x = b->luts;
@@ -439,6 +465,8 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     sp.bcf = bcf;
     sp.negz2 = kNegZero2;
     sp.one2 = kOne2;
+    sp.dq_fast = deq_split(b->act[QMB_ACT_X], &sp.dq_x_hi, &sp.dq_x_lo) &&
+                 deq_split(b->act[QMB_ACT_DT], &sp.dq_dt_hi, &sp.dq_dt_lo);
     sp.h = decode ? ssm_state : ssm_state_out;
     sp.h_in = decode ? 1 : 0;
     sp.h_out = (decode || ssm_state_out) ? 1 : 0;

@@ -4,6 +4,8 @@
 #include <cudaTypedefs.h>
 #include <stdio.h>
 #include <string.h>
+#include <climits>
+#include <stdlib.h>
 #include <mutex>
 
 #include "qmb_gemm.cuh"
@@ -20,11 +22,17 @@ namespace qmb {
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 128;  // bytes of K per stage = one 128B swizzle atom
 
-template <int BN, int EPIW, bool TMAOUT>
+// CG = 2: CTA pair (cluster of 2, tcgen05 cta_group::2): the pair computes a
+// 256 x BN tile; each CTA stages its own 128 rows of A and half (BN/2 rows) of
+// B, the leader issues M=256 MMAs over both CTAs' shared memory, and each CTA's
+// TMEM receives its 128 rows of the accumulator.  Per output element the
+// operand bytes streamed from L2 drop from K(1/BN + 1/128) to K(1/BN + 1/256)
+// x ... per CTA (half of B), which is what bounds the large in/out_proj GEMMs.
+template <int BN, int EPIW, bool TMAOUT, int CG = 1>
 struct TcCfg {
   static constexpr int THREADS = 64 + 32 * EPIW;
   static constexpr int A_BYTES = TC_BM * TC_BK;
-  static constexpr int B_BYTES = BN * TC_BK;
+  static constexpr int B_BYTES = (BN / CG) * TC_BK;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STG_BYTES = TMAOUT ? EPIW * 4096 : 0;  // 2 x (32 rows x 64 B) per epilogue warp
   static constexpr int BUDGET = 230 * 1024 - 1024 - STG_BYTES - 1024;
@@ -45,18 +53,11 @@ __device__ __forceinline__ int epi_quant(float v, const EpiSeg& g, const float* 
   return quant_fast(v, g.out_div, g.out_inv, qmax, err);
 }
 
-// Rare fix-up of a softplus chunk: redo the elements outside the table's
-// verified domain with the exact formula.
-static __device__ __noinline__ void epi_softplus_fix(const float (&v)[32], const EpiSeg& g, const float* qtab,
-                                                     int qmax, uint32_t& err, uint32_t (&packed)[8]) {
-  const float lo = qtab[QTAB_LO], hi = qtab[QTAB_HI];
-#pragma unroll 1
-  for (int j = 0; j < 32; ++j) {
-    if (!softplus_table_miss(v[j], lo, hi)) continue;
-    const int q = softplus_quant_exact(v[j], g.out_div, qmax, &err);
-    const int sh = 8 * (j & 3);
-    packed[j >> 2] = (packed[j >> 2] & ~(0xffu << sh)) | ((uint32_t)(q & 0xff) << sh);
-  }
+// Rare fix-up of one softplus element outside the table's verified domain:
+// the exact formula, out of line (scalar argument, so the caller's chunk stays
+// in registers).
+__device__ __forceinline__ int epi_softplus_fix1(float v, float s_div, int qmax) {
+  return softplus_quant_exact(v, s_div, qmax);  // INT_MIN: non-finite (error word set by the caller)
 }
 
 // 32 epilogue values -> 32 int8 (packed little-endian)
@@ -83,7 +84,20 @@ __device__ __forceinline__ void epi_quant32(const float (&v)[32], const EpiSeg& 
 #pragma unroll
         for (int j = 0; j < 32; ++j) miss |= (v[j] >= lo && v[j] <= hi);
       }
-      if (miss) epi_softplus_fix(v, g, qtab, qmax, err, packed);
+      if (miss) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (softplus_table_miss(v[j], lo, hi)) {
+            int q = epi_softplus_fix1(v[j], g.out_div, qmax);
+            if (q == INT_MIN) {
+              err |= QMB_ERR_NONFINITE;
+              q = 0;
+            }
+            const int sh = 8 * (j & 3);
+            packed[j >> 2] = (packed[j >> 2] & ~(0xffu << sh)) | ((uint32_t)(q & 0xff) << sh);
+          }
+        }
+      }
       return;
     }
   }
@@ -100,10 +114,16 @@ __device__ __forceinline__ void epi_quant32(const float (&v)[32], const EpiSeg& 
 }
 
 // Ragged / misaligned chunk (segment boundary inside the chunk, tails, odd
-// strides): element-wise stores.  Out of line: it is the cold path.
+// strides): element-wise stores.  Out of line: it is the cold path.  It
+// re-reads the chunk from TMEM itself (all 32 lanes call it: tcgen05.ld is
+// warp-collective), so the hot path never has to materialize its registers
+// in local memory for it.
 template <bool SP>
-__device__ __noinline__ void epi_chunk_scalar(const EpiParams& ep, const uint32_t (&r)[32], int nb, int N,
-                                              long long m, const float* qtab, uint32_t& err) {
+__device__ __noinline__ uint32_t epi_chunk_scalar(const EpiParams& ep, uint32_t taddr, int nb, int N, long long m,
+                                                  int M, const float* qtab) {
+  uint32_t r[32], err = 0;
+  tmem_ld_32x32b_x32(taddr, r);
+  if (m >= M) return 0;
 #pragma unroll 1
   for (int j = 0; j < 32; ++j) {
     const int n = nb + j;
@@ -112,19 +132,23 @@ __device__ __noinline__ void epi_chunk_scalar(const EpiParams& ep, const uint32_
     float v = __fmul_rn(__int2float_rn((int)r[j]), sj.acc_scale);
     if (sj.bias) v = __fadd_rn(v, sj.bias[n - sj.n0]);
     const long long off = m * sj.ld + (n - sj.n0);
-    if (sj.kind == EPI_F32)
-      static_cast<float*>(sj.out)[off] = v;
+    if (epi_is_f32(sj.kind))
+      static_cast<float*>(sj.out)[off] = sj.kind == EPI_F32_SILU ? silu_f32_fast(v) : v;
     else
       static_cast<int8_t*>(sj.out)[off] = (int8_t)epi_quant<SP>(v, sj, qtab, ep.qmax, err);
   }
+  return err;
 }
 
-template <int BN, int EPIW, bool TMAOUT>
-__global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
+template <int BN, int EPIW, bool TMAOUT, int CG = 1>
+__global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
     gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2, int M,
                       int N, int Kp, const __grid_constant__ EpiParams ep) {
-  using C = TcCfg<BN, EPIW, TMAOUT>;
+  using C = TcCfg<BN, EPIW, TMAOUT, CG>;
+  constexpr int TILE_M = TC_BM * CG;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;  // CTA's row half of the pair tile
+  const bool leader = rank == 0;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned by offsetting the shared array itself (keeps LDS/STS addressing)
@@ -148,12 +172,12 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
     if (TMAOUT && ep.tma_seg >= 0) tma_prefetch_desc(&tmC);
     if (TMAOUT && ep.tma_seg2 >= 0) tma_prefetch_desc(&tmC2);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], CG);  // (pair: used in the leader only; one arrive per CTA)
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 32 * EPIW);
+      mbar_init(&tempty[b], EPIW * CG);  // one per epilogue warp (pair: the leader's counts both CTAs')
     }
     fence_barrier_init();
   }
@@ -163,13 +187,21 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
     if (ep.seg[s].kind == EPI_SOFTPLUS_Q) qtab_g = ep.seg[s].qtab;
   if (qtab_g)
     for (int k = threadIdx.x; k < QTAB_FLOATS; k += blockDim.x) sQtab[k] = qtab_g[k];
-  if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
+  if (warp == 1) {
+    if (CG == 2)
+      tmem_alloc_pair(tslot, C::TMEM_COLS);
+    else
+      tmem_alloc(tslot, C::TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();  // peer barriers initialized before any remote arrive / TMA completion
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
-  const int num_m = (M + TC_BM - 1) / TC_BM;
+  const int num_m = (M + TILE_M - 1) / TILE_M;
   const int num_n = (N + BN - 1) / BN;
   const int splitk = ep.splitk > 1 ? ep.splitk : 1;
   const int num_tiles = num_m * num_n * splitk;
@@ -178,7 +210,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
   // tile -> (m block, n block, K split): splits of one output tile are adjacent
   auto tile_coords = [&](int tile, int& m0, int& n0, int& kb0, int& kb1) {
     const int sk = tile % splitk, mn = tile / splitk;
-    m0 = (mn / num_n) * TC_BM;
+    m0 = (mn / num_n) * TILE_M;
     n0 = (mn % num_n) * BN;
     kb0 = sk * kper;
     kb1 = min(num_k_all, kb0 + kper);
@@ -189,14 +221,24 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG) {
         int m0, n0, kb0, kb1;
         tile_coords(tile, m0, n0, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait_sleep(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * TC_BK, m0);
-          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * TC_BK, n0);
+          if (CG == 2) {
+            // both CTAs' bytes complete on the leader's barrier
+            if (leader)
+              mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            else
+              mbar_arrive_remote(&full[stage], 0);
+            tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * TC_BK, m0 + (int)rank * TC_BM);
+            tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * TC_BK, n0 + (int)rank * (BN / 2));
+          } else {
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * TC_BK, m0);
+            tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * TC_BK, n0);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -206,12 +248,12 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_i8(TC_BM, BN);
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = umma_idesc_i8(TILE_M, BN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG, ++it) {
         const int buf = it & 1;
         const uint32_t use = (uint32_t)(it >> 1);
         mbar_wait_sleep(&tempty[buf], (use & 1) ^ 1);
@@ -226,16 +268,26 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < TC_BK / 32; ++k) {
-            umma_i8(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                    (kb > kb0 || k > 0) ? 1u : 0u);
+            if (CG == 2)
+              umma_i8_pair(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                           (kb > kb0 || k > 0) ? 1u : 0u);
+            else
+              umma_i8(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                      (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty[stage]);
+          if (CG == 2)
+            umma_commit_pair(&empty[stage]);
+          else
+            umma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[buf]);
+        if (CG == 2)
+          umma_commit_pair(&tfull[buf]);
+        else
+          umma_commit(&tfull[buf]);
       }
     }
   } else {
@@ -251,11 +303,12 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
     const float* qtab = qtab_g ? sQtab : nullptr;
     uint32_t err = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG, ++it) {
       const int buf = it & 1;
       const uint32_t use = (uint32_t)(it >> 1);
       int m0, n0, kb0, kb1;
       tile_coords(tile, m0, n0, kb0, kb1);
+      m0 += (int)rank * TC_BM;  // this CTA's rows of the pair tile
       mbar_wait_sleep(&tfull[buf], use & 1);
       tc_fence_after();
       const long long m = (long long)m0 + row;
@@ -274,7 +327,9 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
               for (int j = 0; j < 32; j += 4)
                 *reinterpret_cast<int4*>(dst + j) = make_int4((int)r[j], (int)r[j + 1], (int)r[j + 2], (int)r[j + 3]);
             } else {
-              for (int j = 0; j < 32 && nb + j < N; ++j) dst[j] = (int)r[j];
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (nb + j < N) dst[j] = (int)r[j];
             }
           }
           continue;
@@ -299,7 +354,11 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
               v[j + 3] = __fadd_rn(v[j + 3], bb.w);
             }
           }
-          if (sg.kind == EPI_F32) {
+          if (epi_is_f32(sg.kind)) {
+            if (sg.kind == EPI_F32_SILU) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = silu_f32_fast(v[j]);
+            }
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
 #pragma unroll
@@ -340,12 +399,16 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
           }
           continue;
         }
-        if (m >= M) continue;
-        const bool f32out = sg.kind == EPI_F32;
+        const bool f32out = epi_is_f32(sg.kind);
         const long long ldb_bytes = sg.ld * (f32out ? 4 : 1);
         const bool fast = (nb + 32 <= sg.n1) && (nb + 32 <= N) && ((sg.n0 & 15) == 0) && (ldb_bytes % 16 == 0) &&
                           ((reinterpret_cast<uintptr_t>(sg.out) & 15) == 0);
-        if (fast) {
+        if (!fast) {  // warp-uniform
+          err |= epi_chunk_scalar<EPIW == 16>(ep, tcol + c * 32, nb, N, m, M, qtab);
+          continue;
+        }
+        if (m >= M) continue;
+        {
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__int2float_rn((int)r[j]), sg.acc_scale);
@@ -361,6 +424,10 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
             }
           }
           if (f32out) {
+            if (sg.kind == EPI_F32_SILU) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = silu_f32_fast(v[j]);
+            }
             float4* o = reinterpret_cast<float4*>(static_cast<float*>(sg.out) + m * sg.ld + (nb - sg.n0));
 #pragma unroll
             for (int j = 0; j < 32; j += 4) o[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
@@ -371,25 +438,32 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT>::THREADS, 1)
             o[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
             o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
           }
-        } else {
-          uint32_t rr[32];  // copy: passing r itself by reference would pin it to local memory
-#pragma unroll
-          for (int j = 0; j < 32; ++j) rr[j] = r[j];
-          epi_chunk_scalar<EPIW == 16>(ep, rr, nb, N, m, qtab, err);
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[buf]);
+      __syncwarp();
+      if (lane == 0) {  // one arrive per epilogue warp (all its TMEM loads have completed)
+        if (CG == 2 && !leader)
+          mbar_arrive_remote(&tempty[buf], 0);
+        else
+          mbar_arrive(&tempty[buf]);
+      }
     }
     if (TMAOUT && lane == 0) bulk_wait0();
     flag_error(ep.err, err);
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();  // no CTA of the pair leaves while remote arrivals / MMAs may still target it
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tbase, C::TMEM_COLS);
+    if (CG == 2)
+      tmem_dealloc_pair(tbase, C::TMEM_COLS);
+    else
+      tmem_dealloc(tbase, C::TMEM_COLS);
   }
 }
 
@@ -552,7 +626,7 @@ int num_sms() {
 static bool make_tmap_store(CUtensorMap* tm, const EpiSeg& s, long long rows) {
   auto enc = get_encode_fn();
   if (!enc) return false;
-  const bool f32 = s.kind == EPI_F32;
+  const bool f32 = epi_is_f32(s.kind);
   cuuint64_t gdim[2] = {(cuuint64_t)(s.n1 - s.n0), (cuuint64_t)rows};
   cuuint64_t gstride[1] = {(cuuint64_t)(s.ld * (f32 ? 4 : 1))};
   cuuint32_t box[2] = {f32 ? 16u : 32u, 32};
@@ -564,17 +638,17 @@ static bool make_tmap_store(CUtensorMap* tm, const EpiSeg& s, long long rows) {
 }
 
 static bool tma_storable(const EpiSeg& g) {
-  const long long eb = g.kind == EPI_F32 ? 4 : 1;
+  const long long eb = epi_is_f32(g.kind) ? 4 : 1;
   return (g.n0 % 32) == 0 && ((g.ld * eb) % 16) == 0 && ((uintptr_t)g.out % 16) == 0 && g.n1 - g.n0 >= 32;
 }
 
-template <int BN, int EPIW, bool TMAOUT>
+template <int BN, int EPIW, bool TMAOUT, int CG = 1>
 static cudaError_t launch_tc(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
                              EpiParams ep, cudaStream_t st) {
-  using C = TcCfg<BN, EPIW, TMAOUT>;
+  using C = TcCfg<BN, EPIW, TMAOUT, CG>;
   CUtensorMap tmA, tmB, tmC, tmC2;
   if (!make_tmap_i8(&tmA, A, M, Kp, lda, TC_BK, TC_BM)) return cudaErrorInvalidValue;
-  if (!make_tmap_i8(&tmB, Bt, N, Kp, ldb, TC_BK, BN)) return cudaErrorInvalidValue;
+  if (!make_tmap_i8(&tmB, Bt, N, Kp, ldb, TC_BK, BN / CG)) return cudaErrorInvalidValue;
   memset(&tmC, 0, sizeof(tmC));
   memset(&tmC2, 0, sizeof(tmC2));
   if (TMAOUT) {
@@ -585,18 +659,42 @@ static cudaError_t launch_tc(const int8_t* A, long long lda, const int8_t* Bt, l
   }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc_kernel<BN, EPIW, TMAOUT>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc_kernel<BN, EPIW, TMAOUT, CG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN) * (ep.splitk > 1 ? ep.splitk : 1);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_i8_tc_kernel<BN, EPIW, TMAOUT><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(tmA, tmB, tmC, tmC2, M, N, Kp, ep);
-  return cudaGetLastError();
+  const int tiles = ((M + TC_BM * CG - 1) / (TC_BM * CG)) * ((N + BN - 1) / BN) * (ep.splitk > 1 ? ep.splitk : 1);
+  const int slots = num_sms() / CG;
+  const int grid = (tiles < slots ? tiles : slots) * CG;
+  if (CG == 1) {
+    gemm_i8_tc_kernel<BN, EPIW, TMAOUT, CG><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(tmA, tmB, tmC, tmC2, M, N, Kp, ep);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_i8_tc_kernel<BN, EPIW, TMAOUT, CG>, tmA, tmB, tmC, tmC2, M, N, Kp, ep);
 }
-
-template <int BN>
+// QMB_GEMM_PAIR=1 enables the CTA-pair kernel (A/B measurements; off by default
+// until it beats the single-CTA kernel).
+static bool gemm_pair_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("QMB_GEMM_PAIR");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+template <int BN, int CG = 1>
 static cudaError_t launch_tc_bn(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
                                 EpiParams ep, cudaStream_t st) {
   bool heavy = false;
@@ -612,11 +710,11 @@ static cudaError_t launch_tc_bn(const int8_t* A, long long lda, const int8_t* Bt
   }
   const bool tma = ep.tma_seg >= 0;
   if (heavy) {
-    if (tma) return launch_tc<BN, 16, true>(A, lda, Bt, ldb, M, N, Kp, ep, st);
-    return launch_tc<BN, 16, false>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    if (tma) return launch_tc<BN, 16, true, CG>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    return launch_tc<BN, 16, false, CG>(A, lda, Bt, ldb, M, N, Kp, ep, st);
   }
-  if (tma) return launch_tc<BN, 8, true>(A, lda, Bt, ldb, M, N, Kp, ep, st);
-  return launch_tc<BN, 8, false>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+  if (tma) return launch_tc<BN, 8, true, CG>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+  return launch_tc<BN, 8, false, CG>(A, lda, Bt, ldb, M, N, Kp, ep, st);
 }
 
 cudaError_t measure_i8_peak(int iters, double* tops) {
@@ -677,6 +775,10 @@ cudaError_t gemm_bench(int M, int N, int K, int mode, int iters, float* ms_out) 
     ep.nseg = 2;
     ep.seg[0] = EpiSeg{0, N / 2, EPI_QUANT, 1e-3f, 0.05f, C, N / 2, nullptr};
     ep.seg[1] = EpiSeg{N / 2, N, EPI_F32, 1e-3f, 1.0f, static_cast<char*>(C) + (size_t)M * N, N / 2, nullptr};
+  } else if (mode == 5) {  // in_proj with the gate's silu(z) in the epilogue
+    ep.nseg = 2;
+    ep.seg[0] = EpiSeg{0, N / 2, EPI_QUANT, 1e-3f, 0.05f, C, N / 2, nullptr};
+    ep.seg[1] = EpiSeg{N / 2, N, EPI_F32_SILU, 1e-3f, 1.0f, static_cast<char*>(C) + (size_t)M * N, N / 2, nullptr};
   } else {
     ep.seg[0] = EpiSeg{0, N, EPI_SOFTPLUS_Q, 1e-3f, 0.01f, C, N, nullptr, tab};
   }
@@ -719,6 +821,8 @@ __global__ void epi_apply_kernel(const int32_t* __restrict__ acc, int splitk, in
   }
   flag_error(ep.err, err);
 }
+
+
 
 template <int BN>
 static cudaError_t launch_tc_choose(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N,
@@ -770,6 +874,9 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
     if (N <= 128) return launch_tc_choose<128>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
     if (N <= 192) return launch_tc_choose<192>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
     const long long m_tiles = (M + TC_BM - 1) / TC_BM;
+    // CTA pairs (256 x 256 tiles) once there are enough pair tiles for every SM pair
+    if (gemm_pair_enabled() && ((M + 255) / 256) * ((N + 255) / 256) >= num_sms() / 2)
+      return launch_tc_bn<256, 2>(A, lda, Bt, ldb, M, N, Kp, ep, st);
     if (m_tiles * ((N + 255) / 256) >= num_sms())
       return launch_tc_choose<256>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
     if (m_tiles * ((N + 127) / 128) >= num_sms())

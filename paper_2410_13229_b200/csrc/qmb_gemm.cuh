@@ -8,6 +8,7 @@
 // steps in the reference's order (int32 -> f32 RN, * f32 scale, + f32 bias,
 // optional softplus, quantize).
 #pragma once
+#include <climits>
 #include <cuda.h>
 
 #include "qmb_common.cuh"
@@ -17,8 +18,10 @@ namespace qmb {
 enum EpiKind : int {
   EPI_QUANT = 0,     // int8 out = quantize(f32(acc) * s [+ bias])
   EPI_F32 = 1,       // f32 out = f32(acc) * s [+ bias]
-  EPI_SOFTPLUS_Q = 2  // int8 out = quantize(softplus(f32(acc) * s [+ bias]))
+  EPI_SOFTPLUS_Q = 2,  // int8 out = quantize(softplus(f32(acc) * s [+ bias]))
+  EPI_F32_SILU = 3     // f32 out = silu(f32(acc) * s [+ bias]) (the gate's silu(z), ssm.py:110-111)
 };
+__host__ __device__ __forceinline__ bool epi_is_f32(int kind) { return kind == EPI_F32 || kind == EPI_F32_SILU; }
 
 struct EpiSeg {
   int n0, n1;           // column range [n0, n1) of the GEMM output this segment covers
@@ -59,15 +62,24 @@ __device__ __forceinline__ bool softplus_table_miss(float v, float lo, float hi)
   return !(fabsf(v) <= 3.402823466e38f) || (v >= lo && v <= hi);
 }
 
-static __device__ __noinline__ int softplus_quant_exact(float v, float s_div, int qmax, uint32_t* err) {
-  return quant_i8(softplus_f32(v), s_div, qmax, *err);
+// Exact path (out of line).  Returns INT_MIN for a non-finite input: no pointer
+// argument, so callers keep their error word in a register.
+static __device__ __noinline__ int softplus_quant_exact(float v, float s_div, int qmax) {
+  uint32_t e = 0;
+  const int q = quant_i8(softplus_f32(v), s_div, qmax, e);
+  return e ? INT_MIN : q;
 }
 
 __device__ __forceinline__ int softplus_quant(float v, const float* __restrict__ qtab, float s_div, float s_inv,
                                               int qmax, uint32_t& err) {
   if (qtab && !softplus_table_miss(v, qtab[QTAB_LO], qtab[QTAB_HI]))
     return softplus_quant_table(v, qtab, s_inv, (float)qmax);
-  return softplus_quant_exact(v, s_div, qmax, &err);
+  const int q = softplus_quant_exact(v, s_div, qmax);
+  if (q == INT_MIN) {
+    err |= QMB_ERR_NONFINITE;
+    return 0;
+  }
+  return q;
 }
 
 struct EpiParams {
@@ -101,8 +113,8 @@ __device__ __forceinline__ void epi_store_one(const EpiParams& ep, const EpiSeg&
   float v = __fmul_rn(__int2float_rn(acc), sg.acc_scale);
   if (sg.bias) v = __fadd_rn(v, sg.bias[n - sg.n0]);
   long long off = m * sg.ld + (n - sg.n0);
-  if (sg.kind == EPI_F32) {
-    static_cast<float*>(sg.out)[off] = v;
+  if (epi_is_f32(sg.kind)) {
+    static_cast<float*>(sg.out)[off] = sg.kind == EPI_F32_SILU ? silu_f32_fast(v) : v;
   } else if (sg.kind == EPI_SOFTPLUS_Q) {
     static_cast<int8_t*>(sg.out)[off] = (int8_t)softplus_quant(v, sg.qtab, sg.out_div, sg.out_inv, ep.qmax, err);
   } else {

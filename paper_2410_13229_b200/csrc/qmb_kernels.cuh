@@ -63,7 +63,10 @@ struct ConvParams {
   float s_out;           // f32(s_out)
   int qmax;
   uint32_t* err;
+  float inv_out, silu_thr;  // set by conv_silu_quant (1 / s_out; verified fast-path threshold)
 };
+// Verified fast-path threshold of quantize(silu(v), s_out) (cached per scale).
+float silu_quant_thr(float s_out, int qmax, cudaStream_t st);
 cudaError_t conv_silu_quant(const ConvParams& p, cudaStream_t st);
 // Decode step: state [B, K-1, C] (in/out), x [B, C] new row -> out [B, C].
 cudaError_t conv_step(const int8_t* x, long long ldx, int8_t* state, const int8_t* w, const float* bias,
@@ -106,6 +109,11 @@ struct ScanParams {
   // exactly rounded product and fma.rn.f32x2(a, ONE, c) an exactly rounded sum; being
   // opaque to ptxas they cannot be folded/contracted (literal constants would be).
   unsigned long long negz2, one2;
+  // dequantization of x / dt as fma(q, hi, q * lo) (3 ALU ops instead of a table
+  // gather); dq_fast is set only when the host verified it equals
+  // f32(f64(q) * s) for every q in [-128, 127] (deq_split in qmb_block.cu)
+  float dq_x_hi, dq_x_lo, dq_dt_hi, dq_dt_lo;
+  int dq_fast;
   float* h;                           // [B, E, N] carried state (in if h_in, out if h_out)
   int h_in, h_out;
   int B, T, E, N;

@@ -71,7 +71,8 @@ def test_quantize_random_bit_exact(cuda, oracle):
 
 @pytest.mark.parametrize("path", [1, 2])
 @pytest.mark.parametrize("M,K,N", [(1, 1, 1), (5, 7, 3), (16, 16, 16), (37, 200, 50), (130, 256, 300),
-                                   (256, 2560, 192), (300, 160, 640), (129, 5120, 96)])
+                                   (256, 2560, 192), (300, 160, 640), (129, 5120, 96), (4100, 400, 1300),
+                                   (2600, 2560, 2100)])
 def test_qlinear_bit_exact(cuda, oracle, path, M, K, N):
     from paper_2410_13229_b200 import QTensor, qlinear
 
@@ -100,7 +101,8 @@ def test_qlinear_known_answers(cuda):
         qlinear(QTensor(np.zeros((1, 2**15 + 1), np.int8), 1.0), QTensor(np.zeros((2**15 + 1, 1), np.int8), 1.0))
 
 
-@pytest.mark.parametrize("T,C,K", [(12, 6, 4), (5, 2, 3), (64, 96, 4), (33, 160, 4), (7, 48, 2), (200, 512, 4)])
+@pytest.mark.parametrize("T,C,K", [(12, 6, 4), (5, 2, 3), (64, 96, 4), (33, 160, 4), (7, 48, 2), (200, 512, 4),
+                                   (37, 64, 3), (3, 32, 4), (1, 16, 4), (21, 32, 5)])
 def test_fused_qconv_bit_exact(cuda, oracle, T, C, K):
     from paper_2410_13229_b200 import QTensor, fused_qconv
 
