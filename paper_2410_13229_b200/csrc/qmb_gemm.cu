@@ -313,10 +313,23 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
       tc_fence_after();
       const long long m = (long long)m0 + row;
       const uint32_t tcol = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN);
+      // 8 epilogue warps (up to 232 registers): the next chunk's TMEM load is in
+      // flight while this one is processed; 16 warps (<= 112 registers): plain loads
+      constexpr bool PF = EPIW <= 8;
+      const int c_beg = part * CH_PER, c_end = min(CHUNKS, (part + 1) * CH_PER);
+      uint32_t rn[32];
+      if (PF && c_beg < c_end) tmem_ld_32x32b_x32_nowait(tcol + c_beg * 32, rn);
 #pragma unroll 1
-      for (int c = part * CH_PER; c < CHUNKS && c < (part + 1) * CH_PER; ++c) {
+      for (int c = c_beg; c < c_end; ++c) {
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tcol + c * 32, r);
+        if (PF) {
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = rn[j];
+          if (c + 1 < c_end) tmem_ld_32x32b_x32_nowait(tcol + (c + 1) * 32, rn);
+        } else {
+          tmem_ld_32x32b_x32(tcol + c * 32, r);
+        }
         const int nb = n0 + c * 32;
         if (nb >= N) continue;  // warp-uniform
         if (splitk > 1) {       // split-K partial -> acc32[split][M][N]; summed (exactly) afterwards
@@ -355,7 +368,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             }
           }
           if (epi_is_f32(sg.kind)) {
-            if (sg.kind == EPI_F32_SILU) {
+            if (EPIW <= 8 && sg.kind == EPI_F32_SILU) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = silu_f32_fast(v[j]);
             }
@@ -404,6 +417,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
         const bool fast = (nb + 32 <= sg.n1) && (nb + 32 <= N) && ((sg.n0 & 15) == 0) && (ldb_bytes % 16 == 0) &&
                           ((reinterpret_cast<uintptr_t>(sg.out) & 15) == 0);
         if (!fast) {  // warp-uniform
+          tmem_wait_ld();  // the prefetched registers must be final before a call may save them
           err |= epi_chunk_scalar<EPIW == 16>(ep, tcol + c * 32, nb, N, m, M, qtab);
           continue;
         }
@@ -424,7 +438,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             }
           }
           if (f32out) {
-            if (sg.kind == EPI_F32_SILU) {
+            if (EPIW <= 8 && sg.kind == EPI_F32_SILU) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = silu_f32_fast(v[j]);
             }
@@ -685,12 +699,11 @@ static cudaError_t launch_tc(const int8_t* A, long long lda, const int8_t* Bt, l
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, gemm_i8_tc_kernel<BN, EPIW, TMAOUT, CG>, tmA, tmB, tmC, tmC2, M, N, Kp, ep);
 }
-// QMB_GEMM_PAIR=1 enables the CTA-pair kernel (A/B measurements; off by default
-// until it beats the single-CTA kernel).
+// QMB_GEMM_PAIR=0 disables the CTA-pair kernel (A/B measurements).
 static bool gemm_pair_enabled() {
   static const bool v = [] {
     const char* e = getenv("QMB_GEMM_PAIR");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return v;
 }
@@ -701,6 +714,7 @@ static cudaError_t launch_tc_bn(const int8_t* A, long long lda, const int8_t* Bt
   ep.tma_seg = ep.tma_seg2 = -1;
   for (int s = 0; s < ep.nseg; ++s) {
     const EpiSeg& g = ep.seg[s];
+    // (silu(z) stays on 8 warps: measured faster than 16, whose register budget spills it)
     if (g.kind == EPI_SOFTPLUS_Q) heavy = true;
     if (!tma_storable(g)) continue;
     if (ep.tma_seg < 0)
@@ -710,6 +724,8 @@ static cudaError_t launch_tc_bn(const int8_t* A, long long lda, const int8_t* Bt
   }
   const bool tma = ep.tma_seg >= 0;
   if (heavy) {
+    for (int s = 0; s < ep.nseg; ++s)
+      if (ep.seg[s].kind == EPI_F32_SILU) return cudaErrorNotSupported;  // silu is compiled for 8 warps only
     if (tma) return launch_tc<BN, 16, true, CG>(A, lda, Bt, ldb, M, N, Kp, ep, st);
     return launch_tc<BN, 16, false, CG>(A, lda, Bt, ldb, M, N, Kp, ep, st);
   }
