@@ -307,9 +307,19 @@ def run_ours(args):
         per[n] = {"ms": round(acc[i], 4), "bound": bound, "achieved": ach, "unit": unit, "frac": ach / peak}
     dom = max(per, key=lambda k: per[k]["ms"])
     d = per[dom]
+    # measured DRAM traffic per launch (ncu --set full, tools/ncu_layer.sh -> profiles/), in the same
+    # unit as `achieved` x seconds: bytes for HBM-bound kernels
+    traffic = None
+    try:
+        tr = json.loads((ROOT / "profiles" / "dram_traffic.json").read_text())
+        if dom in tr.get("kernels", {}):
+            traffic = tr["kernels"][dom]["dram_bytes"]
+    except Exception:
+        pass
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"],
                 "peak": peak_i8.value if d["bound"] == "tensor" else hbm, "unit": d["unit"], "frac": d["frac"],
-                "traffic": None,
+                "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
+                "algorithmic_bytes": (work[dom][1] * 1e9 if d["bound"] == "hbm" else None),
                 "peak_source": ("measured tcgen05 kind::i8 probe (qmb_measure_i8_peak)" if d["bound"] == "tensor"
                                 else "MEASURED_PEAKS.json hbm_gbs"),
                 "per_kernel": per}
@@ -328,7 +338,9 @@ def run_ours(args):
                            "l2": "inputs larger than L2 (per-layer activations >= 1.3 GB)",
                            "step": "embed + 64x(rmsnorm+block) + final norm + last-position LM head + argmax"},
                 "e2e": e2e, "decode": decode, "roofline": roofline, "cpu_baseline": cpu,
-                "clocks": clk.summary(), "gpu_launches": 2 + 8 * cfg.n_layers,
+                # ours per step: embed + 64 x (rmsnorm, in_proj, conv, x_proj, dt_proj, bc_dequant, scan,
+                # hadamard, out_proj) + final norm (the cuBLAS LM head and torch argmax are not counted)
+                "clocks": clk.summary(), "gpu_launches": 2 + 9 * cfg.n_layers,
                 "int8_peak_tops": peak_i8.value, "build_s": round(t_build, 1)}
         print(json.dumps(line), flush=True)
     if world > 1:

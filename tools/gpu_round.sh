@@ -1,3 +1,5 @@
+#!/bin/bash
+# Full round evidence: GPU tests, smoke, bench line, per-layer stage times, launch list, per-kernel ncu.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
