@@ -65,6 +65,7 @@ inline bool deq_split(double s, float* hi, float* lo) {
 
 struct qmb_block {
   int D, E, N, Kc, R, bits, qmax, mode;
+  int in_il;  // in_proj output columns x | z interleaved in blocks of in_il (0: not interleaved)
   int Dp, Ep, Rp, Nx;
   bool had;
   int had_p, had_m;
@@ -166,9 +167,18 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
   b->Nx = 2 * N + R;
 
   // ---- host-side repack into kernel layouts (K-major B operands, padded K)
+  // in_proj columns interleaved x | z in blocks of 64 when E allows, so every
+  // 256-column output tile carries half quantize and half silu epilogue work
+  b->in_il = (E % 64 == 0) ? 64 : 0;
   std::vector<int8_t> w_in_t((size_t)2 * E * b->Dp, 0);
-  for (int k = 0; k < D; ++k)
-    for (int n = 0; n < 2 * E; ++n) w_in_t[(size_t)n * b->Dp + k] = d->w_in.data[(size_t)k * 2 * E + n];
+  for (int n = 0; n < 2 * E; ++n) {
+    int src = n;  // reference column of GEMM column n
+    if (b->in_il) {
+      const int blk = n / b->in_il;
+      src = (blk & 1) * E + (blk >> 1) * b->in_il + (n - blk * b->in_il);
+    }
+    for (int k = 0; k < D; ++k) w_in_t[(size_t)n * b->Dp + k] = d->w_in.data[(size_t)k * 2 * E + src];
+  }
   std::vector<int8_t> w_x_t((size_t)b->Nx * b->Ep, 0);
   for (int k = 0; k < E; ++k) {
     for (int n = 0; n < N; ++n) {
@@ -379,6 +389,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     ep.nseg = 2;
     ep.qmax = b->qmax;
     ep.err = err;
+    ep.il = b->in_il;
     const float s_lin = f32(s_u * b->s_w_in);
     ep.seg[0] = EpiSeg{0, E, EPI_QUANT, s_lin, f32(b->act[QMB_ACT_CONV_IN]), xq, E, nullptr};
     // z-half: silu(z) (the gate's factor, ssm.py:110-111) is computed here, in

@@ -60,6 +60,58 @@ __device__ __forceinline__ int epi_softplus_fix1(float v, float s_div, int qmax)
   return softplus_quant_exact(v, s_div, qmax);  // INT_MIN: non-finite (error word set by the caller)
 }
 
+// silu of 32 epilogue values: branch-free core, one warp-uniform test, and the
+// rare out-of-range inputs (|x| > 80, |x| < 2^-60, non-finite) redone exactly.
+__device__ __forceinline__ void epi_silu32(float (&v)[32]) {
+  uint32_t bad = 0;
+  float y[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    y[j] = silu_core(v[j]);
+    bad |= silu_core_ok(v[j]) ? 0u : (1u << j);
+  }
+  if (bad) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (bad & (1u << j)) y[j] = silu_f32_cold(v[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = y[j];
+}
+
+// quantize 32 values (quant_fast semantics) into packed int8, branch-free except
+// for one test; near-tie / non-finite elements take the exact division.
+__device__ __forceinline__ void epi_quant32_plain(const float (&v)[32], float s, float inv, int qmax, uint32_t& err,
+                                                  uint32_t (&packed)[8]) {
+  const float hi = (float)qmax;
+  uint32_t miss = 0;
+  int q[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float y = __fmul_rn(v[j], inv);
+    const float r = rintf(y);
+    miss |= (fabsf(__fsub_rn(y, r)) < 0.499755859375f) ? 0u : (1u << j);
+    q[j] = (int)fminf(fmaxf(r, -hi), hi);
+  }
+  if (miss) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (miss & (1u << j)) {
+        float r = quant_slow_rint(v[j], s);
+        if (r != r) {
+          err |= QMB_ERR_NONFINITE;
+          r = 0.0f;
+        }
+        q[j] = (int)fminf(fmaxf(r, -hi), hi);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 32; j += 4)
+    packed[j / 4] = (uint32_t)(q[j] & 0xff) | ((uint32_t)(q[j + 1] & 0xff) << 8) | ((uint32_t)(q[j + 2] & 0xff) << 16) |
+                    ((uint32_t)(q[j + 3] & 0xff) << 24);
+}
+
 // 32 epilogue values -> 32 int8 (packed little-endian)
 template <bool SP>
 __device__ __forceinline__ void epi_quant32(const float (&v)[32], const EpiSeg& g, const float* qtab, int qmax,
@@ -101,16 +153,20 @@ __device__ __forceinline__ void epi_quant32(const float (&v)[32], const EpiSeg& 
       return;
     }
   }
+  if (SP) {  // 16-warp kernels (<= 112 registers): per-element form
 #pragma unroll
-  for (int j = 0; j < 32; j += 4) {
-    uint32_t w = 0;
+    for (int j = 0; j < 32; j += 4) {
+      uint32_t w = 0;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int q = epi_quant<SP>(v[j + t], g, qtab, qmax, err);
-      w |= ((uint32_t)(q & 0xff)) << (8 * t);
+      for (int t = 0; t < 4; ++t) {
+        const int q = epi_quant<SP>(v[j + t], g, qtab, qmax, err);
+        w |= ((uint32_t)(q & 0xff)) << (8 * t);
+      }
+      packed[j / 4] = w;
     }
-    packed[j / 4] = w;
+    return;
   }
+  epi_quant32_plain(v, g.out_div, g.out_inv, qmax, err, packed);
 }
 
 // Ragged / misaligned chunk (segment boundary inside the chunk, tails, odd
@@ -128,10 +184,11 @@ __device__ __noinline__ uint32_t epi_chunk_scalar(const EpiParams& ep, uint32_t 
   for (int j = 0; j < 32; ++j) {
     const int n = nb + j;
     if (n >= N) break;
-    const EpiSeg sj = pick_seg(ep, find_seg(ep, n));
+    int oc;
+    const EpiSeg sj = pick_seg(ep, epi_locate(ep, n, &oc));
     float v = __fmul_rn(__int2float_rn((int)r[j]), sj.acc_scale);
-    if (sj.bias) v = __fadd_rn(v, sj.bias[n - sj.n0]);
-    const long long off = m * sj.ld + (n - sj.n0);
+    if (sj.bias) v = __fadd_rn(v, sj.bias[oc]);
+    const long long off = m * sj.ld + oc;
     if (epi_is_f32(sj.kind))
       static_cast<float*>(sj.out)[off] = sj.kind == EPI_F32_SILU ? silu_f32_fast(v) : v;
     else
@@ -298,7 +355,6 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
     constexpr int PARTS = EPIW / 4;
     const int row = quarter * 32 + lane;
     constexpr int CHUNKS = BN / 32;
-    constexpr int CH_PER = (CHUNKS + PARTS - 1) / PARTS;
     float* stg = reinterpret_cast<float*>(sStg + (TMAOUT ? ew * 4096 : 0));
     const float* qtab = qtab_g ? sQtab : nullptr;
     uint32_t err = 0;
@@ -315,18 +371,19 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
       const uint32_t tcol = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN);
       // 8 epilogue warps (up to 232 registers): the next chunk's TMEM load is in
       // flight while this one is processed; 16 warps (<= 112 registers): plain loads
+      // The PARTS warps of a lane quarter take alternating 32-column chunks (so an
+      // interleaved two-segment tile, ep.il, gives each the same mix of work).
       constexpr bool PF = EPIW <= 8;
-      const int c_beg = part * CH_PER, c_end = min(CHUNKS, (part + 1) * CH_PER);
       uint32_t rn[32];
-      if (PF && c_beg < c_end) tmem_ld_32x32b_x32_nowait(tcol + c_beg * 32, rn);
+      if (PF && part < CHUNKS) tmem_ld_32x32b_x32_nowait(tcol + part * 32, rn);
 #pragma unroll 1
-      for (int c = c_beg; c < c_end; ++c) {
+      for (int c = part; c < CHUNKS; c += PARTS) {
         uint32_t r[32];
         if (PF) {
           tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = rn[j];
-          if (c + 1 < c_end) tmem_ld_32x32b_x32_nowait(tcol + (c + 1) * 32, rn);
+          if (c + PARTS < CHUNKS) tmem_ld_32x32b_x32_nowait(tcol + (c + PARTS) * 32, rn);
         } else {
           tmem_ld_32x32b_x32(tcol + c * 32, r);
         }
@@ -347,17 +404,19 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
           }
           continue;
         }
-        const int s = find_seg(ep, nb);
+        int oc;  // output column of this chunk within its segment
+        const int s = epi_locate(ep, nb, &oc);
         const EpiSeg sg = pick_seg(ep, s);
+        const int segw = sg.n1 - sg.n0;
         const int slot = TMAOUT ? (s == ep.tma_seg ? 0 : (s == ep.tma_seg2 ? 1 : -1)) : -1;
-        if (TMAOUT && slot >= 0 && nb + 32 <= sg.n1 && nb + 32 <= N) {
+        if (TMAOUT && slot >= 0 && oc + 32 <= segw && nb + 32 <= N) {
           // 32 rows x 32 cols through swizzled smem -> TMA store (rows >= M are clipped by TMA)
           const CUtensorMap* map = slot == 0 ? &tmC : &tmC2;
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__int2float_rn((int)r[j]), sg.acc_scale);
           if (sg.bias) {
-            const float4* bp = reinterpret_cast<const float4*>(sg.bias + (nb - sg.n0));
+            const float4* bp = reinterpret_cast<const float4*>(sg.bias + oc);
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
               const float4 bb = __ldg(bp + j / 4);
@@ -368,10 +427,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             }
           }
           if (epi_is_f32(sg.kind)) {
-            if (EPIW <= 8 && sg.kind == EPI_F32_SILU) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = silu_f32_fast(v[j]);
-            }
+            if (EPIW <= 8 && sg.kind == EPI_F32_SILU) epi_silu32(v);
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
 #pragma unroll
@@ -387,8 +443,8 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(map, stg, nb - sg.n0, m0 + quarter * 32);
-              tma_store_2d(map, stg + 512, nb - sg.n0 + 16, m0 + quarter * 32);
+              tma_store_2d(map, stg, oc, m0 + quarter * 32);
+              tma_store_2d(map, stg + 512, oc + 16, m0 + quarter * 32);
               bulk_commit();
             }
           } else {
@@ -406,7 +462,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(map, hb, nb - sg.n0, m0 + quarter * 32);
+              tma_store_2d(map, hb, oc, m0 + quarter * 32);
               bulk_commit();
             }
           }
@@ -414,7 +470,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
         }
         const bool f32out = epi_is_f32(sg.kind);
         const long long ldb_bytes = sg.ld * (f32out ? 4 : 1);
-        const bool fast = (nb + 32 <= sg.n1) && (nb + 32 <= N) && ((sg.n0 & 15) == 0) && (ldb_bytes % 16 == 0) &&
+        const bool fast = (oc + 32 <= segw) && (nb + 32 <= N) && ((oc & 15) == 0) && (ldb_bytes % 16 == 0) &&
                           ((reinterpret_cast<uintptr_t>(sg.out) & 15) == 0);
         if (!fast) {  // warp-uniform
           tmem_wait_ld();  // the prefetched registers must be final before a call may save them
@@ -427,7 +483,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__int2float_rn((int)r[j]), sg.acc_scale);
           if (sg.bias) {
-            const float4* bp = reinterpret_cast<const float4*>(sg.bias + (nb - sg.n0));
+            const float4* bp = reinterpret_cast<const float4*>(sg.bias + oc);
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
               const float4 bb = __ldg(bp + j / 4);
@@ -438,17 +494,14 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             }
           }
           if (f32out) {
-            if (EPIW <= 8 && sg.kind == EPI_F32_SILU) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = silu_f32_fast(v[j]);
-            }
-            float4* o = reinterpret_cast<float4*>(static_cast<float*>(sg.out) + m * sg.ld + (nb - sg.n0));
+            if (EPIW <= 8 && sg.kind == EPI_F32_SILU) epi_silu32(v);
+            float4* o = reinterpret_cast<float4*>(static_cast<float*>(sg.out) + m * sg.ld + oc);
 #pragma unroll
             for (int j = 0; j < 32; j += 4) o[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
           } else {
             uint32_t packed[8];
             epi_quant32<EPIW == 16>(v, sg, qtab, ep.qmax, err, packed);
-            uint4* o = reinterpret_cast<uint4*>(static_cast<int8_t*>(sg.out) + m * sg.ld + (nb - sg.n0));
+            uint4* o = reinterpret_cast<uint4*>(static_cast<int8_t*>(sg.out) + m * sg.ld + oc);
             o[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
             o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
           }
@@ -529,10 +582,11 @@ __global__ void __launch_bounds__(256) gemm_i8_simt_kernel(const int8_t* __restr
     for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
   }
   uint32_t err = 0;
-  const EpiSeg sg = pick_seg(ep, find_seg(ep, n));
+  int oc;
+  const EpiSeg sg = pick_seg(ep, epi_locate(ep, n, &oc));
 #pragma unroll
   for (int i = 0; i < MB; ++i) {
-    if (lane == i && m0 + i < M) epi_store_one(ep, sg, m0 + i, n, acc[i], err);
+    if (lane == i && m0 + i < M) epi_store_one(ep, sg, m0 + i, oc, acc[i], err);
   }
   flag_error(ep.err, err);
 }
@@ -833,7 +887,9 @@ __global__ void epi_apply_kernel(const int32_t* __restrict__ acc, int splitk, in
     const int n = (int)(k - m * N);
     int s = 0;
     for (int sk = 0; sk < splitk; ++sk) s += acc[sk * total + k];  // int32: exact in any order
-    epi_store_one(ep, pick_seg(ep, find_seg(ep, n)), m, n, s, err);
+    int oc;
+    const EpiSeg sg = pick_seg(ep, epi_locate(ep, n, &oc));
+    epi_store_one(ep, sg, m, oc, s, err);
   }
   flag_error(ep.err, err);
 }

@@ -89,6 +89,8 @@ struct EpiParams {
   EpiSeg seg[3];
   int tma_seg;   // segments written through TMA store maps tmC / tmC2 (set by gemm_i8), or -1
   int tma_seg2;
+  int il;          // > 0: GEMM columns interleave two segments in blocks of il columns
+                   // (block b -> segment b & 1, output column (b >> 1) * il + offset)
   int splitk;      // > 1: split-K over K blocks; partial int32 sums stored per split
   int32_t* acc32;  // [splitk, M, N] int32 partials; a second kernel sums them and runs the epilogue
 };
@@ -107,12 +109,25 @@ __device__ __forceinline__ int find_seg(const EpiParams& ep, int n) {
   return s;
 }
 
-// One output element, scalar path (shared by the SIMT kernel and ragged tiles).
-__device__ __forceinline__ void epi_store_one(const EpiParams& ep, const EpiSeg& sg, long long m, int n, int acc,
+// GEMM column n -> (segment, output column within the segment)
+__device__ __forceinline__ int epi_locate(const EpiParams& ep, int n, int* ocol) {
+  if (ep.il > 0) {
+    const int blk = n / ep.il;
+    *ocol = (blk >> 1) * ep.il + (n - blk * ep.il);
+    return blk & 1;
+  }
+  const int s = find_seg(ep, n);
+  *ocol = n - pick_seg(ep, s).n0;
+  return s;
+}
+
+// One output element, scalar path (shared by the SIMT kernel and ragged tiles);
+// oc = output column within segment sg.
+__device__ __forceinline__ void epi_store_one(const EpiParams& ep, const EpiSeg& sg, long long m, int oc, int acc,
                                               uint32_t& err) {
   float v = __fmul_rn(__int2float_rn(acc), sg.acc_scale);
-  if (sg.bias) v = __fadd_rn(v, sg.bias[n - sg.n0]);
-  long long off = m * sg.ld + (n - sg.n0);
+  if (sg.bias) v = __fadd_rn(v, sg.bias[oc]);
+  long long off = m * sg.ld + oc;
   if (epi_is_f32(sg.kind)) {
     static_cast<float*>(sg.out)[off] = sg.kind == EPI_F32_SILU ? silu_f32_fast(v) : v;
   } else if (sg.kind == EPI_SOFTPLUS_Q) {
