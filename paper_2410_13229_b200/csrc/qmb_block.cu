@@ -84,6 +84,7 @@ struct qmb_block {
   uint8_t* a_col;   // [E, N]
   float* exp_lut;   // [128, exp_ncols]
   int exp_ncols;
+  float* exp_tab;   // [E, 128, N] expf(deq_dt[level] * a[i][j]) (N == 16 only; else null)
   float* d_deq;     // [E]
   int8_t* w_out_t;  // [D, Ep]
   float* luts;      // [4][256] dequant tables: x, dt, b, c (index q + 128)
@@ -231,7 +232,8 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
                o_wdt = take(w_dt_t.size()), o_dtb = take(E * 4), o_a = take((size_t)E * N * 4),
                o_acol = take((size_t)E * N), o_lut = take((size_t)128 * b->exp_ncols * 4), o_d = take(E * 4),
                o_wo = take(w_out_t.size()), o_luts = take(4 * 256 * 4), o_avals = take(a_vals.size() * 4),
-               o_qtab = take(QTAB_FLOATS * 4), o_scr = take(16);
+               o_qtab = take(QTAB_FLOATS * 4), o_scr = take(16),
+               o_etab = take(N == 16 ? (size_t)E * 128 * 16 * 4 : 0);
   cudaError_t e = cudaMalloc(&b->mem, off);
   if (e != cudaSuccess) {
     delete b;
@@ -247,6 +249,7 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
   b->a_deq = (float*)(base + o_a);
   b->a_col = (uint8_t*)(base + o_acol);
   b->exp_lut = (float*)(base + o_lut);
+  b->exp_tab = N == 16 ? (float*)(base + o_etab) : nullptr;
   b->d_deq = (float*)(base + o_d);
   b->w_out_t = (int8_t*)(base + o_wo);
   b->luts = (float*)(base + o_luts);
@@ -274,6 +277,7 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
     }
   }
   e = build_exp_lut(b->luts + 256, avals_dev, b->exp_ncols, b->exp_lut, 0);
+  if (e == cudaSuccess && b->exp_tab) e = build_exp_tab(b->luts + 256, b->a_deq, E, b->exp_tab, 0);
   if (e == cudaSuccess) e = build_softplus_qtab(f32(d->act[QMB_ACT_DT]), b->qmax, b->sp_qtab, scratch, 0);
   // verified conv silu+quantize fast path for this layer's scale (cached)
   if (e == cudaSuccess) (void)silu_quant_thr(f32(d->act[QMB_ACT_X]), b->qmax, 0);
@@ -328,6 +332,18 @@ extern "C" int qmb_block_workspace_layout(const qmb_block* b, long long rows, si
   ws_layout(b, rows, offsets, &total);
   return 0;
 }
+// Decode scan: each channel-step reads its 16 exps as one row of the layer's
+// resident exp table (3, default); QMB_DECODE_SCAN=0 evaluates the exact expf
+// directly in FP64, =2 gathers the compact (level, a-value) table through L1.
+static int decode_scan_mode() {
+  static const int v = [] {
+    const char* e = getenv("QMB_DECODE_SCAN");
+    if (e && (e[0] == '0' || e[0] == '2')) return e[0] - '0';
+    return 3;  // rows of the resident exp table
+  }();
+  return v;
+}
+
 // Where the gate's silu(z) is evaluated: the in_proj epilogue (default) or the
 // scan (QMB_ZSILU_IN_GEMM=0, kept for A/B measurements).  Same f32 values either way.
 static bool zsilu_in_gemm() {
@@ -472,6 +488,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     sp.a_col = b->a_col;
     sp.exp_lut = b->exp_lut;
     sp.exp_ncols = b->exp_ncols;
+    sp.exp_tab = b->exp_tab;
     sp.d = b->d_deq;
     sp.bcf = bcf;
     sp.negz2 = kNegZero2;
@@ -488,7 +505,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     sp.err = err;
     // 1: tabulated expf in shared memory (prefill), 2: tabulated expf through L1
     // (decode, one step per sequence), 0: direct FP64 glibc-expf restatement
-    const int use_lut = scan_exp != 0 ? 0 : (decode ? 2 : 1);
+    const int use_lut = scan_exp != 0 ? 0 : (decode ? decode_scan_mode() : 1);
     QMB_CUDA(selective_scan(sp, use_lut, st), "scan");
   }
   // output quantization (qblock.py:211-214)
@@ -618,7 +635,9 @@ __global__ void dequant_kernel(const int8_t* q, int n, double s, float* out) {
 
 extern "C" size_t qmb_qlinear_workspace_bytes(long long M, int K, int N) {
   const long long Kp = round_up(K, 16);
-  return (size_t)(round_up(M * Kp, 256) + round_up((long long)N * Kp, 256) + round_up((long long)N * 4, 256));
+  // + split-K scratch for decode-size M
+  return (size_t)(round_up(M * Kp, 256) + round_up((long long)N * Kp, 256) + round_up((long long)N * 4, 256) +
+                  (M <= 64 ? SPLITK_SCRATCH_INTS * 4 : 0));
 }
 
 extern "C" int qmb_qlinear(const int8_t* x_q, long long M, int K, double s_x, const int8_t* w_q, int N, double s_w,
@@ -656,7 +675,10 @@ extern "C" int qmb_qlinear(const int8_t* x_q, long long M, int K, double s_x, co
     ep.seg[0] = EpiSeg{0, N, EPI_QUANT, acc_scale, f32(s_out), out, N, bias_q ? bias : nullptr};
   else
     ep.seg[0] = EpiSeg{0, N, EPI_F32, acc_scale, 1.0f, out, N, bias_q ? bias : nullptr};
-  QMB_CUDA(gemm_i8(A, lda, bt, Kp, (int)M, N, K, ep, st, path), "qlinear gemm");
+  int32_t* acc32 = nullptr;
+  if (M <= 64)  // split-K scratch for decode-size M
+    acc32 = (int32_t*)(w + round_up(M * Kp, 256) + round_up((long long)N * Kp, 256) + round_up((long long)N * 4, 256));
+  QMB_CUDA(gemm_i8(A, lda, bt, Kp, (int)M, N, K, ep, st, path, acc32), "qlinear gemm");
   return 0;
 }
 

@@ -103,6 +103,7 @@ struct ScanParams {
   const float* a;                     // [E, N] dequantized a (direct-exp path)
   const uint8_t* a_col;               // [E, N] column into exp_lut (LUT path)
   const float* exp_lut; int exp_ncols;  // [128][exp_ncols]: expf(deq_dt[q] * a_col value), q in [0,127]
+  const float* exp_tab;               // [E, 128, 16] per-channel expf rows (d_state 16) or nullptr
   const float* d;                     // [E] dequantized d
   float* bcf;                         // [B*T, 2N] scratch for dequantized b | c rows (batch-tiled scan), or null
   // {-0.0f, -0.0f} and {1.0f, 1.0f} as runtime operands: fma.rn.f32x2(a, b, NEGZ) is an
@@ -122,6 +123,10 @@ struct ScanParams {
 // use_lut: 1 = per-layer expf table in shared memory (prefill kernels), 2 = same
 // table read through L1 (decode), 0 = direct FP64 glibc-expf restatement.
 cudaError_t selective_scan(const ScanParams& p, int use_lut, cudaStream_t st);
+// exp_tab[(i * 128 + r) * 16 + j] = glibc_expf(lut_dt[r + 128] * a[i * 16 + j]) (the layer's
+// per-channel exp rows, resident with the block handle: decode reads a row per
+// channel-step, prefill CTAs copy their 16 channels into shared memory)
+cudaError_t build_exp_tab(const float* lut_dt, const float* a, int E, float* exp_tab, cudaStream_t st);
 // exp_lut[r * ncols + c] = glibc_expf(lut_dt[r + 128] * a_vals[c]) for r in [0, 127]
 cudaError_t build_exp_lut(const float* lut_dt, const float* a_vals, int ncols, float* exp_lut, cudaStream_t st);
 

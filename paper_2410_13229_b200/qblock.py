@@ -199,7 +199,8 @@ def _finish(t: torch.Tensor, as_numpy: bool):
 
 
 def qlinear(x_q, w_q, bias_q=None, s_out: float | None = None, extra_scale: float = 1.0, *, path: int = 0):
-    """qblock.py:98-123 on the tensor cores (path 1) or the GEMV kernel (path 2)."""
+    """qblock.py:98-123 on the tensor cores (path 1) or the dp4a GEMV kernel (path 2);
+    path 0 picks by shape."""
     if x_q.zero_point or w_q.zero_point:
         raise ValueError("qlinear requires symmetric operands")
     d_in = w_q.values.shape[0]
