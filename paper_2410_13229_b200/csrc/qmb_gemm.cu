@@ -35,7 +35,7 @@ struct TcCfg {
   static constexpr int B_BYTES = (BN / CG) * TC_BK;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STG_BYTES = TMAOUT ? EPIW * 4096 : 0;  // 2 x (32 rows x 64 B) per epilogue warp
-  static constexpr int BUDGET = 230 * 1024 - 1024 - STG_BYTES - 1024;
+  static constexpr int BUDGET = 227 * 1024 - 1024 - STG_BYTES - 1024;  // (227 KB: the per-CTA opt-in maximum)
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS =
       (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
@@ -62,15 +62,17 @@ __device__ __forceinline__ int epi_softplus_fix1(float v, float s_div, int qmax)
 
 // silu of 32 epilogue values: branch-free core, one warp-uniform test, and the
 // rare out-of-range inputs (|x| > 80, |x| < 2^-60, non-finite) redone exactly.
-__device__ __forceinline__ void epi_silu32(float (&v)[32]) {
+// Rows past M (the zero-filled tail of a partial tile, e.g. a decode batch) are
+// never stored, so their out-of-range zeros skip the fix-up.
+__device__ __forceinline__ void epi_silu32(float (&v)[32], bool row_valid) {
   uint32_t bad = 0;
   float y[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
-    // silu(+-0) = +-0 / 2 = +-0 (zero rows of a partial tile land here too)
-    y[j] = v[j] == 0.0f ? v[j] : silu_core(v[j]);
-    bad |= (silu_core_ok(v[j]) || v[j] == 0.0f) ? 0u : (1u << j);
+    y[j] = silu_core(v[j]);
+    bad |= silu_core_ok(v[j]) ? 0u : (1u << j);
   }
+  if (!row_valid) bad = 0;
   if (bad) {
 #pragma unroll
     for (int j = 0; j < 32; ++j)
@@ -258,6 +260,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
+  pdl_trigger();  // (decode chains: the next kernel may start its prologue)
 
   const int num_m = (M + TILE_M - 1) / TILE_M;
   const int num_n = (N + BN - 1) / BN;
@@ -279,10 +282,32 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // The weights (B) do not depend on the previous kernel: under PDL the first
+      // tile's first STAGES B loads are issued before the dependency wait, their A
+      // halves after it.
+      int pre = 0;
+      if (CG == 1 && (int)blockIdx.x < num_tiles) {
+        int m0, n0, kb0, kb1;
+        tile_coords(blockIdx.x, m0, n0, kb0, kb1);
+        for (int kb = kb0; kb < kb1 && pre < STAGES; ++kb, ++pre) {
+          mbar_arrive_expect_tx(&full[pre], C::STAGE_BYTES);
+          tma_load_2d(sB + pre * C::B_BYTES, &tmB, &full[pre], kb * TC_BK, n0);
+        }
+      }
+      pdl_wait();
+      int it = 0;
       for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG) {
         int m0, n0, kb0, kb1;
         tile_coords(tile, m0, n0, kb0, kb1);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          if (it < pre) {  // B already in flight; stage / phase advance as in the main path
+            tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * TC_BK, m0);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           if (ep.spin) mbar_wait(&empty[stage], phase ^ 1); else mbar_wait_sleep(&empty[stage], phase ^ 1);
           if (CG == 2) {
             // both CTAs' bytes complete on the leader's barrier
@@ -360,6 +385,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
     const float* qtab = qtab_g ? sQtab : nullptr;
     uint32_t err = 0;
     int it = 0;
+    pdl_wait();
     for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG, ++it) {
       const int buf = it & 1;
       const uint32_t use = (uint32_t)(it >> 1);
@@ -428,7 +454,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             }
           }
           if (epi_is_f32(sg.kind)) {
-            if (EPIW <= 8 && sg.kind == EPI_F32_SILU) epi_silu32(v);
+            if (EPIW <= 8 && sg.kind == EPI_F32_SILU) epi_silu32(v, m < M);
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
 #pragma unroll
@@ -495,7 +521,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             }
           }
           if (f32out) {
-            if (EPIW <= 8 && sg.kind == EPI_F32_SILU) epi_silu32(v);
+            if (EPIW <= 8 && sg.kind == EPI_F32_SILU) epi_silu32(v, m < M);
             float4* o = reinterpret_cast<float4*>(static_cast<float*>(sg.out) + m * sg.ld + oc);
 #pragma unroll
             for (int j = 0; j < 32; j += 4) o[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
@@ -736,10 +762,9 @@ static cudaError_t launch_tc(const int8_t* A, long long lda, const int8_t* Bt, l
   const int tiles = ((M + TC_BM * CG - 1) / (TC_BM * CG)) * ((N + BN - 1) / BN) * (ep.splitk > 1 ? ep.splitk : 1);
   const int slots = num_sms() / CG;
   const int grid = (tiles < slots ? tiles : slots) * CG;
-  if (CG == 1) {
-    gemm_i8_tc_kernel<BN, EPIW, TMAOUT, CG><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(tmA, tmB, tmC, tmC2, M, N, Kp, ep);
-    return cudaGetLastError();
-  }
+  if (CG == 1)
+    return launch_pdl(M <= 128, gemm_i8_tc_kernel<BN, EPIW, TMAOUT, CG>, dim3((unsigned)grid), dim3(C::THREADS),
+                      (size_t)C::SMEM_BYTES, st, tmA, tmB, tmC, tmC2, M, N, Kp, ep);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(C::THREADS);
@@ -907,6 +932,8 @@ cudaError_t gemm_bench(int M, int N, int K, int mode, int iters, float* ms_out) 
 // Epilogue of a split-K GEMM: the exact int32 sums in acc32 [M, N] through the
 // same per-element float steps as the fused epilogue.
 __global__ void epi_apply_kernel(const int32_t* __restrict__ acc, int splitk, int M, int N, EpiParams ep) {
+  pdl_wait();
+  pdl_trigger();
   uint32_t err = 0;
   const long long total = (long long)M * N;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
@@ -957,8 +984,8 @@ static cudaError_t launch_tc_choose(const int8_t* A, long long lda, const int8_t
   const long long total = (long long)M * N;
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  epi_apply_kernel<<<(unsigned)blocks, 256, 0, st>>>(acc32, splitk, M, N, ep);
-  return cudaGetLastError();
+  return launch_pdl(true, epi_apply_kernel, dim3((unsigned)blocks), dim3(256), 0, st, (const int32_t*)acc32, splitk, M,
+                    N, ep);
 }
 
 cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
@@ -976,6 +1003,9 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
   if (path == 1 && !tc_ok) return cudaErrorInvalidValue;
   if (path == 1) {
     if (M > TC_BM) acc32 = nullptr;  // split-K only for skinny (decode-like) M
+    // skinny M: one wave of 96-column tiles beats two waves of 64-column ones
+    if (M <= TC_BM && N > 192 && (N + 63) / 64 > num_sms() && (N + 95) / 96 <= num_sms())
+      return launch_tc_choose<96>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
     // Column tile: the largest BN that still gives >= 1 wave, else the smallest.
     if (N <= 32) return launch_tc_choose<32>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
     if (N <= 64) return launch_tc_choose<64>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);

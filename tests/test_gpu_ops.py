@@ -71,6 +71,7 @@ def test_quantize_random_bit_exact(cuda, oracle):
 
 @pytest.mark.parametrize("path", [0, 1, 2])
 @pytest.mark.parametrize("M,K,N", [(1, 1, 1), (5, 7, 3), (16, 16, 16), (37, 200, 50), (130, 256, 300), (64, 2560, 1000),
+                                   (64, 320, 9600), (7, 2560, 10240),
                                    (64, 160, 5120), (33, 5120, 192),
                                    (256, 2560, 192), (300, 160, 640), (129, 5120, 96), (4100, 400, 1300),
                                    (2600, 2560, 2100)])
