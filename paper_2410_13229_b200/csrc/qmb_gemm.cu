@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
       const long long m = (long long)m0 + row;
       const uint32_t tcol = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN);
       // 8 epilogue warps (up to 232 registers): the next chunk's TMEM load is in
-      // flight while this one is processed; 16 warps (<= 112 registers): plain loads
+      // flight while this one is processed; 12 / 16 warps (<= 128 / 112 registers): plain loads
       // The PARTS warps of a lane quarter take alternating 32-column chunks (so an
       // interleaved two-segment tile, ep.il, gives each the same mix of work).
       constexpr bool PF = EPIW <= 8;
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             }
           }
           if (epi_is_f32(sg.kind)) {
-            if (EPIW <= 8 && sg.kind == EPI_F32_SILU) epi_silu32(v, m < M);
+            if (EPIW <= 12 && sg.kind == EPI_F32_SILU) epi_silu32(v, m < M);
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
 #pragma unroll
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             }
           }
           if (f32out) {
-            if (EPIW <= 8 && sg.kind == EPI_F32_SILU) epi_silu32(v, m < M);
+            if (EPIW <= 12 && sg.kind == EPI_F32_SILU) epi_silu32(v, m < M);
             float4* o = reinterpret_cast<float4*>(static_cast<float*>(sg.out) + m * sg.ld + oc);
 #pragma unroll
             for (int j = 0; j < 32; j += 4) o[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
@@ -787,6 +787,14 @@ static bool gemm_pair_enabled() {
   }();
   return v;
 }
+// QMB_SILU12=1: the in_proj silu(z) epilogue on 12 warps instead of 8 (A/B).
+static bool silu12_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("QMB_SILU12");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
 template <int BN, int CG = 1>
 static cudaError_t launch_tc_bn(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
                                 EpiParams ep, cudaStream_t st) {
@@ -808,6 +816,10 @@ static cudaError_t launch_tc_bn(const int8_t* A, long long lda, const int8_t* Bt
       if (ep.seg[s].kind == EPI_F32_SILU) return cudaErrorNotSupported;  // silu is compiled for 8 warps only
     if (tma) return launch_tc<BN, 16, true, CG>(A, lda, Bt, ldb, M, N, Kp, ep, st);
     return launch_tc<BN, 16, false, CG>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+  }
+  if (CG == 2 && tma && silu12_enabled()) {  // the silu(z) epilogue on 12 warps (3 per TMEM lane quarter)
+    for (int s = 0; s < ep.nseg; ++s)
+      if (ep.seg[s].kind == EPI_F32_SILU) return launch_tc<BN, 12, true, CG>(A, lda, Bt, ldb, M, N, Kp, ep, st);
   }
   if (tma) return launch_tc<BN, 8, true, CG>(A, lda, Bt, ldb, M, N, Kp, ep, st);
   return launch_tc<BN, 8, false, CG>(A, lda, Bt, ldb, M, N, Kp, ep, st);
