@@ -125,6 +125,17 @@ int qmb_block_prefill(const qmb_block* blk, const int8_t* u_q, double u_scale, i
                       int8_t* conv_state_out, float* ssm_state_out, int scan_exp,
                       void* workspace, size_t ws_bytes, uint32_t* err_flag, qmb_stream_t stream);
 
+/* Same, accumulating: res[m, :] += block output (bit-identical to the residual
+ * add `x_out + x_res` of the next fused_rmsnorm_quant, qblock.py:181, folded into
+ * out_proj's epilogue; forward_q's loop (model.py:246-258) then normalizes res
+ * directly).  Model-level fusion, not a reference operator. */
+int qmb_block_prefill_accum(const qmb_block* blk, const int8_t* u_q, double u_scale, int B, int T, float* res,
+                            int8_t* conv_state_out, float* ssm_state_out, int scan_exp,
+                            void* workspace, size_t ws_bytes, uint32_t* err_flag, qmb_stream_t stream);
+int qmb_block_decode_accum(const qmb_block* blk, const int8_t* u_q, double u_scale, int B, int8_t* conv_state,
+                           float* ssm_state, float* res, void* workspace, size_t ws_bytes,
+                           uint32_t* err_flag, qmb_stream_t stream);
+
 /* Quantized single-token decode (no reference function: semantics = last row
  * of block_forward_q on the prefix; state carry pinned by test_formats.py:76-94).
  * u_q [B, d_model]; conv_state [B, d_conv-1, d_inner] and ssm_state

@@ -52,6 +52,9 @@ PROTOTYPES = {
     "qmb_block_workspace_layout": (c_int, [c_vp, c_ll, ctypes.POINTER(c_sz)]),
     "qmb_block_prefill": (c_int, [c_vp, c_i8p, c_dbl, c_int, c_int, c_vp, c_i8p, c_vp, c_int, c_vp, c_sz, c_vp, c_vp]),
     "qmb_block_decode": (c_int, [c_vp, c_i8p, c_dbl, c_int, c_i8p, c_vp, c_vp, c_vp, c_sz, c_vp, c_vp]),
+    "qmb_block_prefill_accum": (c_int, [c_vp, c_i8p, c_dbl, c_int, c_int, c_vp, c_i8p, c_vp, c_int, c_vp, c_sz, c_vp,
+                                        c_vp]),
+    "qmb_block_decode_accum": (c_int, [c_vp, c_i8p, c_dbl, c_int, c_i8p, c_vp, c_vp, c_vp, c_sz, c_vp, c_vp]),
     "qmb_block_prefill_profiled": (c_int, [c_vp, c_i8p, c_dbl, c_int, c_int, c_vp, c_int, c_vp, c_sz, c_vp, c_vp,
                                            ctypes.POINTER(ctypes.c_float)]),
     "qmb_rmsnorm_residual_quant":(c_int, [c_vp, c_vp, c_vp, c_vp, c_ll, c_int, c_dbl, c_int, c_i8p, c_vp, c_vp,

@@ -367,7 +367,7 @@ static thread_local cudaEvent_t* g_prof = nullptr;
 // carried conv window and h).
 static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int B, int T, float* out, int8_t* conv_state,
                      float* ssm_state, bool decode, int8_t* conv_state_out, float* ssm_state_out, int scan_exp,
-                     void* ws, size_t ws_bytes, uint32_t* err, cudaStream_t st) {
+                     void* ws, size_t ws_bytes, uint32_t* err, cudaStream_t st, bool accum = false) {
   if (!b || !u_q || !out) return fail(QMB_E_ARG, "null argument");
   if (B < 0 || T < 0) return fail(QMB_E_ARG, "batch and length must be non-negative");
   const long long M = (long long)B * T;
@@ -537,7 +537,8 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     ep.err = err;
     const double s_y = b->had ? b->act[QMB_ACT_Y_HAD] : b->act[QMB_ACT_Y];
     const double extra = b->had ? 1.0 / (double)E : 1.0;
-    ep.seg[0] = EpiSeg{0, D, EPI_F32, f32(s_y * b->s_w_out * extra), 1.0f, out, D, nullptr};
+    // accum: out += the block output (the next fused_rmsnorm_quant's residual add, qblock.py:181)
+    ep.seg[0] = EpiSeg{0, D, accum ? EPI_F32_ADDTO : EPI_F32, f32(s_y * b->s_w_out * extra), 1.0f, out, D, nullptr};
     QMB_CUDA(gemm_i8(yq, b->Ep, b->w_out_t, b->Ep, (int)M, D, E, ep, st, 0, acc32), "out_proj gemm");
   }
   PROF(7, st);
@@ -566,6 +567,21 @@ extern "C" int qmb_block_prefill(const qmb_block* b, const int8_t* u_q, double u
                                  size_t ws_bytes, uint32_t* err, qmb_stream_t stream) {
   return block_run(b, u_q, u_scale, B, T, out, nullptr, nullptr, false, conv_state_out, ssm_state_out, scan_exp, ws,
                    ws_bytes, err, (cudaStream_t)stream);
+}
+
+extern "C" int qmb_block_prefill_accum(const qmb_block* b, const int8_t* u_q, double u_scale, int B, int T,
+                                       float* res, int8_t* conv_state_out, float* ssm_state_out, int scan_exp,
+                                       void* ws, size_t ws_bytes, uint32_t* err, qmb_stream_t stream) {
+  return block_run(b, u_q, u_scale, B, T, res, nullptr, nullptr, false, conv_state_out, ssm_state_out, scan_exp, ws,
+                   ws_bytes, err, (cudaStream_t)stream, true);
+}
+
+extern "C" int qmb_block_decode_accum(const qmb_block* b, const int8_t* u_q, double u_scale, int B,
+                                      int8_t* conv_state, float* ssm_state, float* res, void* ws, size_t ws_bytes,
+                                      uint32_t* err, qmb_stream_t stream) {
+  if (!conv_state || !ssm_state) return fail(QMB_E_ARG, "decode requires conv and ssm state");
+  return block_run(b, u_q, u_scale, B, 1, res, conv_state, ssm_state, true, nullptr, nullptr, 0, ws, ws_bytes, err,
+                   (cudaStream_t)stream, true);
 }
 
 extern "C" int qmb_block_decode(const qmb_block* b, const int8_t* u_q, double u_scale, int B, int8_t* conv_state,

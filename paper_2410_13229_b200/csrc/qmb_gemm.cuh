@@ -19,9 +19,13 @@ enum EpiKind : int {
   EPI_QUANT = 0,     // int8 out = quantize(f32(acc) * s [+ bias])
   EPI_F32 = 1,       // f32 out = f32(acc) * s [+ bias]
   EPI_SOFTPLUS_Q = 2,  // int8 out = quantize(softplus(f32(acc) * s [+ bias]))
-  EPI_F32_SILU = 3     // f32 out = silu(f32(acc) * s [+ bias]) (the gate's silu(z), ssm.py:110-111)
+  EPI_F32_SILU = 3,    // f32 out = silu(f32(acc) * s [+ bias]) (the gate's silu(z), ssm.py:110-111)
+  EPI_F32_ADDTO = 4    // f32 out = (f32(acc) * s [+ bias]) + out (the residual add of the next
+                       // fused_rmsnorm_quant, qblock.py:181, folded into out_proj's epilogue)
 };
-__host__ __device__ __forceinline__ bool epi_is_f32(int kind) { return kind == EPI_F32 || kind == EPI_F32_SILU; }
+__host__ __device__ __forceinline__ bool epi_is_f32(int kind) {
+  return kind == EPI_F32 || kind == EPI_F32_SILU || kind == EPI_F32_ADDTO;
+}
 
 struct EpiSeg {
   int n0, n1;           // column range [n0, n1) of the GEMM output this segment covers
@@ -130,7 +134,8 @@ __device__ __forceinline__ void epi_store_one(const EpiParams& ep, const EpiSeg&
   if (sg.bias) v = __fadd_rn(v, sg.bias[oc]);
   long long off = m * sg.ld + oc;
   if (epi_is_f32(sg.kind)) {
-    static_cast<float*>(sg.out)[off] = sg.kind == EPI_F32_SILU ? silu_f32_fast(v) : v;
+    float* o = static_cast<float*>(sg.out) + off;
+    *o = sg.kind == EPI_F32_SILU ? silu_f32_fast(v) : (sg.kind == EPI_F32_ADDTO ? __fadd_rn(v, *o) : v);
   } else if (sg.kind == EPI_SOFTPLUS_Q) {
     static_cast<int8_t*>(sg.out)[off] = (int8_t)softplus_quant(v, sg.qtab, sg.out_div, sg.out_inv, ep.qmax, err);
   } else {

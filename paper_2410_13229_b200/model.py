@@ -123,13 +123,20 @@ class DeviceModel:
         x_res = torch.zeros_like(x_out)
         u_q = torch.empty((M, self.D), dtype=torch.int8, device=x_out.device)
         ws = _device.workspace(max(b.workspace_bytes(M) for b in self.blocks))
+        # The residual stream lives in x_res: layer 0 forms res = emb + 0 (model.py:249-253);
+        # every block then adds its output into x_res in out_proj's epilogue, which is the
+        # next fused_rmsnorm_quant's `x_out + x_res` (qblock.py:181) - so later norms read
+        # the stream directly.
         for li, blk in enumerate(self.blocks):
-            self._rmsnorm(x_out, x_res, x_res, self.norms[li], self.s_in[li], u_q, None, M, err, stream)
+            if li == 0:
+                self._rmsnorm(x_out, x_res, x_res, self.norms[li], self.s_in[li], u_q, None, M, err, stream)
+            else:
+                self._rmsnorm(x_res, None, None, self.norms[li], self.s_in[li], u_q, None, M, err, stream)
             conv, h = states[li] if states is not None else (None, None)
-            blk.prefill(u_q, B, T, x_out, conv_state_out=conv, ssm_state_out=h, scan_exp=scan_exp, workspace=ws,
-                        err=err, stream=stream)
+            blk.prefill(u_q, B, T, x_res, conv_state_out=conv, ssm_state_out=h, scan_exp=scan_exp, workspace=ws,
+                        err=err, stream=stream, accumulate=True)
         final = torch.empty_like(x_out)
-        self._rmsnorm(x_out, x_res, None, self.final_norm, 1.0, None, final, M, err, stream)
+        self._rmsnorm(x_res, None, None, self.final_norm, 1.0, None, final, M, err, stream)
         return final
 
     def forward(self, tokens: torch.Tensor, *, last_only: bool = False, scan_exp: int = 0) -> torch.Tensor:
@@ -163,11 +170,14 @@ class DeviceModel:
         x_out, x_res, u_q, final, ws = bufs
         self.embed(tokens, out=x_out)
         x_res.zero_()
-        for li, blk in enumerate(self.blocks):
-            self._rmsnorm(x_out, x_res, x_res, self.norms[li], self.s_in[li], u_q, None, B, err, stream)
+        for li, blk in enumerate(self.blocks):  # residual stream in x_res, as in forward_hidden
+            if li == 0:
+                self._rmsnorm(x_out, x_res, x_res, self.norms[li], self.s_in[li], u_q, None, B, err, stream)
+            else:
+                self._rmsnorm(x_res, None, None, self.norms[li], self.s_in[li], u_q, None, B, err, stream)
             conv, h = states[li]
-            blk.decode(u_q, conv, h, x_out, workspace=ws, err=err, stream=stream)
-        self._rmsnorm(x_out, x_res, None, self.final_norm, 1.0, None, final, B, err, stream)
+            blk.decode(u_q, conv, h, x_res, workspace=ws, err=err, stream=stream, accumulate=True)
+        self._rmsnorm(x_res, None, None, self.final_norm, 1.0, None, final, B, err, stream)
         return self.lm_head(final)
 
     def decode_buffers(self, B: int):

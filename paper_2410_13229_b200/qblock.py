@@ -155,22 +155,27 @@ class DeviceBlock:
 
     def prefill(self, u_q: torch.Tensor, B: int, T: int, out: torch.Tensor, *, u_scale: float | None = None,
                 conv_state_out=None, ssm_state_out=None, scan_exp: int = 0, workspace=None, err=None,
-                stream: int | None = None) -> torch.Tensor:
+                stream: int | None = None, accumulate: bool = False) -> torch.Tensor:
+        """block_forward_q over B sequences; accumulate=True adds the block output
+        into `out` (the residual stream) instead of overwriting it."""
         M = B * T
         ws = workspace if workspace is not None else _device.workspace(self.workspace_bytes(M))
         e = err if err is not None else _device.err_flag()
-        _lib.check(self._lib.qmb_block_prefill(
+        fn = self._lib.qmb_block_prefill_accum if accumulate else self._lib.qmb_block_prefill
+        _lib.check(fn(
             self.handle, u_q.data_ptr(), float(u_scale or 0.0), int(B), int(T), out.data_ptr(),
             _device.ptr(conv_state_out), _device.ptr(ssm_state_out), int(scan_exp), ws.data_ptr(), ws.numel(),
             e.ptr, stream if stream is not None else _device.stream_ptr()), "qmb_block_prefill")
         return out
 
     def decode(self, u_q: torch.Tensor, conv_state: torch.Tensor, ssm_state: torch.Tensor, out: torch.Tensor, *,
-               u_scale: float | None = None, workspace=None, err=None, stream: int | None = None) -> torch.Tensor:
+               u_scale: float | None = None, workspace=None, err=None, stream: int | None = None,
+               accumulate: bool = False) -> torch.Tensor:
         B = u_q.shape[0]
         ws = workspace if workspace is not None else _device.workspace(self.workspace_bytes(B))
         e = err if err is not None else _device.err_flag()
-        _lib.check(self._lib.qmb_block_decode(
+        fn = self._lib.qmb_block_decode_accum if accumulate else self._lib.qmb_block_decode
+        _lib.check(fn(
             self.handle, u_q.data_ptr(), float(u_scale or 0.0), int(B), conv_state.data_ptr(),
             ssm_state.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(), e.ptr,
             stream if stream is not None else _device.stream_ptr()), "qmb_block_decode")
