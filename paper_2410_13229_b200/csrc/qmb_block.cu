@@ -280,7 +280,12 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
   if (e == cudaSuccess && b->exp_tab) e = build_exp_tab(b->luts + 256, b->a_deq, E, b->exp_tab, 0);
   if (e == cudaSuccess) e = build_softplus_qtab(f32(d->act[QMB_ACT_DT]), b->qmax, b->sp_qtab, scratch, 0);
   // verified conv silu+quantize fast path for this layer's scale (cached)
-  if (e == cudaSuccess) (void)silu_quant_thr(f32(d->act[QMB_ACT_X]), b->qmax, 0);
+  if (e == cudaSuccess) {
+    const float t_silu = silu_quant_thr(f32(d->act[QMB_ACT_X]), b->qmax, 0);
+    if (getenv("QMB_VERBOSE"))
+      fprintf(stderr, "qmb_block_create: verified silu-quant fast-path threshold %.9g (s=%g)\n", t_silu,
+              d->act[QMB_ACT_X]);
+  }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     cudaFree(b->mem);

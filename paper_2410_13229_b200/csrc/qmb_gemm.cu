@@ -443,7 +443,9 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
           const CUtensorMap* map = slot == 0 ? &tmC : &tmC2;
           float v[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__int2float_rn((int)r[j]), sg.acc_scale);
+          for (int j = 0; j < 32; ++j)  // (16-warp softplus kernels: short-K accumulators off the XU)
+            v[j] = __fmul_rn((EPIW == 16 && ep.small_acc) ? i2f_small((int)r[j]) : __int2float_rn((int)r[j]),
+                             sg.acc_scale);
           if (sg.bias) {
             const float4* bp = reinterpret_cast<const float4*>(sg.bias + oc);
 #pragma unroll
@@ -521,7 +523,9 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
         {
           float v[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__int2float_rn((int)r[j]), sg.acc_scale);
+          for (int j = 0; j < 32; ++j)  // (16-warp softplus kernels: short-K accumulators off the XU)
+            v[j] = __fmul_rn((EPIW == 16 && ep.small_acc) ? i2f_small((int)r[j]) : __int2float_rn((int)r[j]),
+                             sg.acc_scale);
           if (sg.bias) {
             const float4* bp = reinterpret_cast<const float4*>(sg.bias + oc);
 #pragma unroll
@@ -1031,6 +1035,7 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
   ep.splitk = 1;
   ep.acc32 = nullptr;
   ep.spin = 0;  // (spinning waits measured no faster for decode-size GEMMs)
+  ep.small_acc = (long long)Kp * 128 * 128 < (1LL << 22) ? 1 : 0;
   for (int s = 0; s < ep.nseg; ++s) ep.seg[s].out_inv = 1.0f / ep.seg[s].out_div;  // RN f32 reciprocal
   const bool tc_ok = (lda % 16 == 0) && (ldb % 16 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)Bt % 16 == 0) &&
                      Kp > 0;

@@ -96,6 +96,7 @@ struct EpiParams {
   int il;          // > 0: GEMM columns interleave two segments in blocks of il columns
                    // (block b -> segment b & 1, output column (b >> 1) * il + offset)
   int spin;        // pipeline waits spin (short, latency-bound GEMMs: decode) instead of sleeping
+  int small_acc;   // |acc| < 2^22 (K < 256): accumulators convert with i2f_small (set by gemm_i8)
   int splitk;      // > 1: split-K over K blocks; partial int32 sums stored per split
   int32_t* acc32;  // [splitk, M, N] int32 partials; a second kernel sums them and runs the epilogue
 };
