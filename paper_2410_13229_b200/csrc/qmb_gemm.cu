@@ -82,19 +82,19 @@ __device__ __forceinline__ void epi_silu32(float (&v)[32], bool row_valid) {
   for (int j = 0; j < 32; ++j) v[j] = y[j];
 }
 
-// quantize 32 values (quant_fast semantics) into packed int8, branch-free except
-// for one test; near-tie / non-finite elements take the exact division.
+// quantize 32 finite values (quant_fast semantics) into packed int8, branch-free
+// except for one test and free of conversion-unit ops; near-tie elements take the
+// exact division.
 __device__ __forceinline__ void epi_quant32_plain(const float (&v)[32], float s, float inv, int qmax, uint32_t& err,
                                                   uint32_t (&packed)[8]) {
   const float hi = (float)qmax;
   uint32_t miss = 0;
   int q[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const float y = __fmul_rn(v[j], inv);
-    const float r = rintf(y);
-    miss |= (fabsf(__fsub_rn(y, r)) < 0.499755859375f) ? 0u : (1u << j);
-    q[j] = (int)fminf(fmaxf(r, -hi), hi);
+  for (int j = 0; j < 32; ++j) {  // (v finite: an int32 accumulator times a finite scale)
+    float d;
+    q[j] = quant_level_magic(__fmul_rn(v[j], inv), hi + 1.0f, qmax, &d);
+    miss |= (d < 0.499755859375f) ? 0u : (1u << j);
   }
   if (miss) {
 #pragma unroll
