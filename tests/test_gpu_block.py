@@ -152,3 +152,36 @@ def test_block_decode_equals_prefill(cuda, name):
     for b in range(B):
         assert np.array_equal(got[b].view(np.uint32), z["st_out"].view(np.uint32)), b
     assert np.array_equal(h[0].cpu().numpy().view(np.uint32), z["st_h"].view(np.uint32))
+
+
+@pytest.mark.parametrize("name", ["m20_full", "p2_naive", "s130m"])
+def test_block_accumulate_is_the_residual_add(cuda, name):
+    """qmb_block_prefill_accum / qmb_block_decode_accum add the block output into a
+    residual buffer in out_proj's epilogue: bit-identical to the f32 add
+    `x_out + x_res` that the next fused_rmsnorm_quant performs (qblock.py:181)."""
+    from paper_2410_13229_b200 import _device
+    from paper_2410_13229_b200.qblock import device_block
+
+    z, meta = load_block(name)
+    qb = mirror_block(z, meta)
+    dev = device_block(qb)
+    rng = np.random.default_rng(11)
+    B, T, D = 3, 9, meta["cfg"]["d_model"]
+    u = torch.from_numpy(rng.integers(-127, 128, size=(B * T, D)).astype(np.int8)).cuda()
+    res0 = rng.standard_normal((B * T, D)).astype(np.float32)
+    out = torch.empty((B * T, D), dtype=torch.float32, device="cuda")
+    dev.prefill(u, B, T, out, u_scale=meta["u_scale"])
+    res = torch.from_numpy(res0).cuda()
+    dev.prefill(u, B, T, res, u_scale=meta["u_scale"], accumulate=True)
+    _device.err_flag().raise_if_set()
+    ref = out.cpu().numpy() + res0
+    assert np.array_equal(res.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    # decode: one step from a fresh state, plain vs accumulated
+    conv, h = dev.new_state(B)
+    conv2, h2 = dev.new_state(B)
+    row = torch.empty((B, D), dtype=torch.float32, device="cuda")
+    dev.decode(u[:B].contiguous(), conv, h, row, u_scale=meta["u_scale"])
+    acc = torch.from_numpy(res0[:B].copy()).cuda()
+    dev.decode(u[:B].contiguous(), conv2, h2, acc, u_scale=meta["u_scale"], accumulate=True)
+    _device.err_flag().raise_if_set()
+    assert np.array_equal(acc.cpu().numpy().view(np.uint32), (row.cpu().numpy() + res0[:B]).view(np.uint32))
