@@ -115,6 +115,111 @@ __device__ __forceinline__ void epi_quant32_plain(const float (&v)[32], float s,
                     ((uint32_t)(q[j + 3] & 0xff) << 24);
 }
 
+// Compact TMA-store chunk (CTA-pair kernels): the 32-column chunk is processed as four
+// 8-column sub-chunks in a rolled loop, each loaded from TMEM, converted, finished
+// (bias, residual add, silu or quantize) and staged, so the per-kind code is a
+// few hundred instructions: with the x and z chunks of a tile interleaved, the
+// fully unrolled 32-wide paths did not fit the instruction cache together.
+__device__ __forceinline__ void epi_silu8(float (&v)[8], bool row_valid) {
+  uint32_t bad = 0;
+  float y[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    y[j] = silu_core(v[j]);
+    bad |= silu_core_ok(v[j]) ? 0u : (1u << j);
+  }
+  if (!row_valid) bad = 0;
+  if (bad) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (bad & (1u << j)) y[j] = silu_f32_cold(v[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = y[j];
+}
+
+template <int EPIW>
+__device__ __forceinline__ void epi_chunk_sub8(const EpiParams& ep, const EpiSeg& sg, uint32_t taddr, float* stg,
+                                               int oc, long long m, int M, int lane, const CUtensorMap* map,
+                                               int row0, uint32_t& err) {
+  const bool f32 = epi_is_f32(sg.kind);
+  const float hi = (float)ep.qmax;
+  if (lane == 0) bulk_wait_read0();  // the staging buffer's previous store has been read
+  __syncwarp();
+  uint8_t* hb8 = reinterpret_cast<uint8_t*>(stg);
+  const int sw32 = (lane >> 2) & 1;
+#pragma unroll 1
+  for (int g = 0; g < 4; ++g) {
+    uint32_t r8[8];
+    tmem_ld_32x32b_x8(taddr + 8 * g, r8);
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __fmul_rn(__int2float_rn((int)r8[j]), sg.acc_scale);
+    if (sg.bias) {
+      const float4* bp = reinterpret_cast<const float4*>(sg.bias + oc + 8 * g);
+      const float4 b0 = __ldg(bp), b1 = __ldg(bp + 1);
+      v[0] = __fadd_rn(v[0], b0.x), v[1] = __fadd_rn(v[1], b0.y), v[2] = __fadd_rn(v[2], b0.z);
+      v[3] = __fadd_rn(v[3], b0.w), v[4] = __fadd_rn(v[4], b1.x), v[5] = __fadd_rn(v[5], b1.y);
+      v[6] = __fadd_rn(v[6], b1.z), v[7] = __fadd_rn(v[7], b1.w);
+    }
+    if (f32) {
+      if (sg.kind == EPI_F32_ADDTO && m < M) {
+        const float4* op = reinterpret_cast<const float4*>(static_cast<const float*>(sg.out) + m * sg.ld + oc + 8 * g);
+        const float4 o0 = op[0], o1 = op[1];
+        v[0] = __fadd_rn(v[0], o0.x), v[1] = __fadd_rn(v[1], o0.y), v[2] = __fadd_rn(v[2], o0.z);
+        v[3] = __fadd_rn(v[3], o0.w), v[4] = __fadd_rn(v[4], o1.x), v[5] = __fadd_rn(v[5], o1.y);
+        v[6] = __fadd_rn(v[6], o1.z), v[7] = __fadd_rn(v[7], o1.w);
+      }
+      if (sg.kind == EPI_F32_SILU) epi_silu8(v, m < M);
+      // 32 rows x 16 floats per half, 64B rows, SWIZZLE_64B: quad q of a row at q ^ ((row >> 1) & 3)
+      float* hb = stg + (g >> 1) * 512;
+      const int qa = (g & 1) * 2;
+      *reinterpret_cast<float4*>(hb + lane * 16 + ((qa ^ ((lane >> 1) & 3)) * 4)) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(hb + lane * 16 + (((qa + 1) ^ ((lane >> 1) & 3)) * 4)) =
+          make_float4(v[4], v[5], v[6], v[7]);
+    } else {  // EPI_QUANT (v finite)
+      uint32_t miss = 0;
+      int q[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float d;
+        q[j] = quant_level_magic(__fmul_rn(v[j], sg.out_inv), hi + 1.0f, ep.qmax, &d);
+        miss |= (d < 0.499755859375f) ? 0u : (1u << j);
+      }
+      if (miss) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (miss & (1u << j)) {
+            float rr = quant_slow_rint(v[j], sg.out_div);
+            if (rr != rr) {
+              err |= QMB_ERR_NONFINITE;
+              rr = 0.0f;
+            }
+            q[j] = (int)fminf(fmaxf(rr, -hi), hi);
+          }
+        }
+      }
+      const uint32_t w0 = (uint32_t)(q[0] & 0xff) | ((uint32_t)(q[1] & 0xff) << 8) | ((uint32_t)(q[2] & 0xff) << 16) |
+                          ((uint32_t)(q[3] & 0xff) << 24);
+      const uint32_t w1 = (uint32_t)(q[4] & 0xff) | ((uint32_t)(q[5] & 0xff) << 8) | ((uint32_t)(q[6] & 0xff) << 16) |
+                          ((uint32_t)(q[7] & 0xff) << 24);
+      // 32 rows x 32 B, SWIZZLE_32B: 16B chunk c of row r at chunk c ^ ((r >> 2) & 1)
+      *reinterpret_cast<uint2*>(hb8 + lane * 32 + (((g >> 1) ^ sw32) * 16) + (g & 1) * 8) = make_uint2(w0, w1);
+    }
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    if (f32) {
+      tma_store_2d(map, stg, oc, row0);
+      tma_store_2d(map, stg + 512, oc + 16, row0);
+    } else {
+      tma_store_2d(map, hb8, oc, row0);
+    }
+    bulk_commit();
+  }
+}
+
 // 32 epilogue values -> 32 int8 (packed little-endian)
 template <bool SP>
 __device__ __forceinline__ void epi_quant32(const float (&v)[32], const EpiSeg& g, const float* qtab, int qmax,
@@ -402,11 +507,26 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
       // flight while this one is processed; 12 / 16 warps (<= 128 / 112 registers): plain loads
       // The PARTS warps of a lane quarter take alternating 32-column chunks (so an
       // interleaved two-segment tile, ep.il, gives each the same mix of work).
-      constexpr bool PF = EPIW <= 8;
+      constexpr bool SUB8 = CG == 2 && TMAOUT && EPIW != 16;  // compact sub-chunk path (epi_chunk_sub8)
+      constexpr bool PF = EPIW <= 8 && !SUB8;
       uint32_t rn[32];
       if (PF && part < CHUNKS) tmem_ld_32x32b_x32_nowait(tcol + part * 32, rn);
 #pragma unroll 1
       for (int c = part; c < CHUNKS; c += PARTS) {
+        if (SUB8 && splitk == 1) {
+          const int nb = n0 + c * 32;
+          if (nb >= N) continue;
+          int oc;
+          const int s = epi_locate(ep, nb, &oc);
+          const EpiSeg sg = pick_seg(ep, s);
+          const int slot = s == ep.tma_seg ? 0 : (s == ep.tma_seg2 ? 1 : -1);
+          if (slot >= 0 && oc + 32 <= sg.n1 - sg.n0 && nb + 32 <= N &&
+              (epi_is_f32(sg.kind) || sg.kind == EPI_QUANT)) {
+            epi_chunk_sub8<EPIW>(ep, sg, tcol + c * 32, stg, oc, m, M, lane, slot == 0 ? &tmC : &tmC2,
+                                 m0 + quarter * 32, err);
+            continue;
+          }
+        }
         uint32_t r[32];
         if (PF) {
           tmem_wait_ld();
