@@ -48,17 +48,20 @@ struct EpiSeg {
 constexpr int QTAB_FLOATS = 131;
 constexpr int QTAB_LO = 129, QTAB_HI = 130;
 
-// The table function: a fast-math estimate q0 of the level, then a +/-1
-// correction from the two thresholds around it (level q <=> tab[q] <= v < tab[q+1]).
-// Branch-free; the sweep verifies exactly this function.
+// The table function: a fast-math estimate of the level, taken half a level low
+// (q0 = rint(sp / s - 1/2) in {q - 1, q} for the true level q), then one threshold
+// comparison lifts it (level q <=> tab[q] <= v < tab[q + 1]).  The rint is the
+// 1.5 * 2^23 bias add (no conversion-unit op).  Branch-free; the sweep verifies
+// exactly this function.
 __device__ __forceinline__ int softplus_quant_table(float v, const float* __restrict__ tab, float s_inv,
                                                     float qmaxf) {
   float e, l;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmul_rn(v, 1.44269504088896341f)));
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(__fadd_rn(1.0f, e)));
   const float sp = v > 15.0f ? v : __fmul_rn(l, 0.693147180559945309f);
-  const int q0 = __float2int_rn(fminf(fmaxf(__fmul_rn(sp, s_inv), 0.0f), qmaxf));
-  return q0 + (v >= tab[q0 + 1] ? 1 : 0) - (v < tab[q0] ? 1 : 0);
+  const float y = fminf(fmaxf(__fmaf_rn(sp, s_inv, -0.5f), 0.0f), qmaxf);
+  const int q0 = __float_as_int(__fadd_rn(y, 12582912.0f)) - 0x4B400000;
+  return q0 + (v >= tab[q0 + 1] ? 1 : 0);
 }
 
 // v needs the exact path (outside the verified domain of the table function)

@@ -179,6 +179,30 @@ def test_hadamard_golden_and_quant(cuda, oracle):
     assert hadamard_quantize(np.array([[64.0, 0, 0, 0]], np.float32), 1.0, plan).values.tolist() == [[64] * 4]
 
 
+@pytest.mark.parametrize("n", [1536, 5120])
+def test_hadamard_quant_ties_clamps_and_nonfinite(cuda, oracle, n):
+    """The packed quantize of the fast Hadamard kernels: exact .5 ties (scalar
+    fallback), values far beyond +-qmax, near-zero rows and a non-finite row."""
+    from paper_2410_13229_b200 import apply_hadamard, hadamard_quantize, plan_for_dim
+
+    plan = plan_for_dim(n)
+    rng = np.random.default_rng(n)
+    y = (rng.standard_normal((6, n)) * 4).astype(np.float32)
+    y[0] = 0.0
+    y[0, 0] = 2.5                      # every output is +-2.5: all ties
+    y[1] = np.float32(0.5) * rng.integers(-9, 10, n).astype(np.float32) / np.float32(np.sqrt(n))
+    y[2] *= np.float32(1e4)            # clamps
+    y[3] *= np.float32(1e-30)          # rounds to 0
+    y[4, ::7] = -0.0
+    h = apply_hadamard(plan, y)
+    for s in (1.0, 0.37, float(np.abs(h[5]).max() / 127)):
+        assert np.array_equal(hadamard_quantize(y, s, plan).values, oracle.quantize(h, s)), s
+    bad = y.copy()
+    bad[5, 17] = np.inf
+    with pytest.raises(ValueError):
+        hadamard_quantize(bad, 1.0, plan)
+
+
 @pytest.mark.parametrize("M,D", [(3, 8), (6, 16), (33, 64), (50, 768), (17, 2560), (9, 1000),
                                  (700, 2560), (640, 768), (1200, 64), (600, 1000)])
 def test_rmsnorm_residual_quant_bit_exact(cuda, oracle, M, D):
