@@ -223,21 +223,21 @@ __device__ __forceinline__ void epi_chunk_sub8(const EpiParams& ep, const EpiSeg
 // 32 epilogue values -> 32 int8 (packed little-endian)
 template <bool SP>
 __device__ __forceinline__ void epi_quant32(const float (&v)[32], const EpiSeg& g, const float* qtab, int qmax,
-                                            uint32_t& err, uint32_t (&packed)[8]) {
+                                            uint32_t& err, uint32_t (&packed)[8], uint32_t qtab_bias) {
   if constexpr (SP) {
     if (g.kind == EPI_SOFTPLUS_Q && qtab) {
       const float lo = qtab[QTAB_LO], hi = qtab[QTAB_HI], qmaxf = (float)qmax;
+      const uint32_t tab_b = softplus_tab_bias(qtab, qtab_bias);
       float chk = 0.0f;  // NaN-sticky: becomes NaN iff some v is not finite
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
-        uint32_t w = 0;
+        uint32_t b[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          const int q = softplus_quant_table(v[j + t], qtab, g.out_inv, qmaxf);
+          b[t] = softplus_quant_table_bits(v[j + t], tab_b, g.out_inv, qmaxf);
           chk = __fmaf_rn(v[j + t], 0.0f, chk);
-          w |= ((uint32_t)(q & 0xff)) << (8 * t);
         }
-        packed[j / 4] = w;
+        packed[j / 4] = __byte_perm(__byte_perm(b[0], b[1], 0x40), __byte_perm(b[2], b[3], 0x40), 0x5410);
       }
       bool miss = !(chk == 0.0f);
       if (lo <= hi) {  // a disagreement interval exists (uniform; typically empty)
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             }
           } else {
             uint32_t packed[8];
-            epi_quant32<EPIW == 16>(v, sg, qtab, ep.qmax, err, packed);
+            epi_quant32<EPIW == 16>(v, sg, qtab, ep.qmax, err, packed, ep.qtab_bias);
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
             // 32 rows x 32 B, SWIZZLE_32B: 16B chunk c of row r at chunk c ^ ((r >> 2) & 1)
@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             for (int j = 0; j < 32; j += 4) o[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
           } else {
             uint32_t packed[8];
-            epi_quant32<EPIW == 16>(v, sg, qtab, ep.qmax, err, packed);
+            epi_quant32<EPIW == 16>(v, sg, qtab, ep.qmax, err, packed, ep.qtab_bias);
             uint4* o = reinterpret_cast<uint4*>(static_cast<int8_t*>(sg.out) + m * sg.ld + oc);
             o[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
             o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
@@ -1156,6 +1156,7 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
   ep.acc32 = nullptr;
   ep.spin = 0;  // (spinning waits measured no faster for decode-size GEMMs)
   ep.small_acc = (long long)Kp * 128 * 128 < (1LL << 22) ? 1 : 0;
+  ep.qtab_bias = QTAB_BIAS;
   for (int s = 0; s < ep.nseg; ++s) ep.seg[s].out_inv = 1.0f / ep.seg[s].out_div;  // RN f32 reciprocal
   const bool tc_ok = (lda % 16 == 0) && (ldb % 16 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)Bt % 16 == 0) &&
                      Kp > 0;

@@ -53,15 +53,29 @@ constexpr int QTAB_LO = 129, QTAB_HI = 130;
 // comparison lifts it (level q <=> tab[q] <= v < tab[q + 1]).  The rint is the
 // 1.5 * 2^23 bias add (no conversion-unit op).  Branch-free; the sweep verifies
 // exactly this function.
-__device__ __forceinline__ int softplus_quant_table(float v, const float* __restrict__ tab, float s_inv,
-                                                    float qmaxf) {
-  float e, l;
+// Returns the level biased by 0x4B400000 (its low byte is the int8 code): the bias
+// add's bits index the table directly (a 32-bit shared-window address,
+// softplus_tab_bias(tab) = addr(tab) + 4 - 4 * 0x4B400000 mod 2^32) and feed the byte
+// packing without an integer conversion.  tab must be in shared memory.
+constexpr uint32_t QTAB_BIAS = 4u - 4u * 0x4B400000u;
+// bias: QTAB_BIAS, passed at run time by the epilogue (EpiParams::qtab_bias) so that
+// ptxas cannot split the constant back off the per-element address
+__device__ __forceinline__ uint32_t softplus_tab_bias(const float* tab, uint32_t bias = QTAB_BIAS) {
+  return (uint32_t)__cvta_generic_to_shared(tab) + bias;
+}
+__device__ __forceinline__ uint32_t softplus_quant_table_bits(float v, uint32_t tab_b, float s_inv, float qmaxf) {
+  float e, l, t;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmul_rn(v, 1.44269504088896341f)));
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(__fadd_rn(1.0f, e)));
   const float sp = v > 15.0f ? v : __fmul_rn(l, 0.693147180559945309f);
   const float y = fminf(fmaxf(__fmaf_rn(sp, s_inv, -0.5f), 0.0f), qmaxf);
-  const int q0 = __float_as_int(__fadd_rn(y, 12582912.0f)) - 0x4B400000;
-  return q0 + (v >= tab[q0 + 1] ? 1 : 0);
+  const uint32_t b = __float_as_uint(__fadd_rn(y, 12582912.0f));
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(tab_b + 4u * b));
+  return b + (v >= t ? 1u : 0u);
+}
+__device__ __forceinline__ int softplus_quant_table(float v, const float* __restrict__ tab, float s_inv,
+                                                    float qmaxf) {
+  return (int)(softplus_quant_table_bits(v, softplus_tab_bias(tab), s_inv, qmaxf) - 0x4B400000u);
 }
 
 // v needs the exact path (outside the verified domain of the table function)
@@ -100,6 +114,7 @@ struct EpiParams {
                    // (block b -> segment b & 1, output column (b >> 1) * il + offset)
   int spin;        // pipeline waits spin (short, latency-bound GEMMs: decode) instead of sleeping
   int small_acc;   // |acc| < 2^22 (K < 256): accumulators convert with i2f_small (set by gemm_i8)
+  uint32_t qtab_bias;  // QTAB_BIAS (set by gemm_i8)
   int splitk;      // > 1: split-K over K blocks; partial int32 sums stored per split
   int32_t* acc32;  // [splitk, M, N] int32 partials; a second kernel sums them and runs the epilogue
 };
