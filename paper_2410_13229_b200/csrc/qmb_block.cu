@@ -556,8 +556,9 @@ extern "C" int qmb_block_prefill_profiled(const qmb_block* b, const int8_t* u_q,
   cudaEvent_t ev[QMB_NUM_STAGES + 1];
   for (int i = 0; i <= QMB_NUM_STAGES; ++i) QMB_CUDA(cudaEventCreate(&ev[i]), "event");
   g_prof = ev;
+  // (accumulating out_proj, as every layer of the model's prefill runs it)
   int rc = block_run(b, u_q, u_scale, B, T, out, nullptr, nullptr, false, nullptr, nullptr, scan_exp, ws, ws_bytes,
-                     err, (cudaStream_t)stream);
+                     err, (cudaStream_t)stream, true);
   g_prof = nullptr;
   if (rc == 0) {
     QMB_CUDA(cudaEventSynchronize(ev[QMB_NUM_STAGES]), "event sync");

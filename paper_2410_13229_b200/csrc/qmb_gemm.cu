@@ -1001,9 +1001,22 @@ cudaError_t measure_i8_peak(int iters, double* tops) {
 // GEMM microbenchmark on synthetic operands (tuning tool): mode 0 = f32 out
 // (TMA store), 1 = int8 requant out, 2 = f32 out without TMA store, 3 = two
 // segments (int8 | f32) like in_proj, 4 = softplus+quant with a dummy table.
+__global__ void bench_fill_kernel(int8_t* p, size_t n, uint32_t seed) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ seed;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    p[i] = (int8_t)(h >> 24);
+  }
+}
+
 cudaError_t gemm_bench(int M, int N, int K, int mode, int iters, float* ms_out) {
   // mode + 10: SIMT GEMV path; mode + 20: tensor-core path with split-K scratch (decode-like);
-  // mode + 100: L2 flushed (256 MB memset) before every timed launch
+  // mode + 100: L2 flushed (256 MB memset) before every timed launch; mode + 1000: random
+  // int8 operands (default: all ones)
+  const bool rnd = mode >= 1000;
+  mode %= 1000;
   const bool cold = mode >= 100;
   mode %= 100;
   const int path = mode >= 10 && mode < 20 ? 2 : 1;
@@ -1022,8 +1035,13 @@ cudaError_t gemm_bench(int M, int N, int K, int mode, int iters, float* ms_out) 
   if (e == cudaSuccess) e = cudaMalloc(&C, (size_t)M * N * 4 + 256);
   if (e == cudaSuccess) e = cudaMalloc(&tab, QTAB_FLOATS * 4);
   if (e != cudaSuccess) return e;
-  cudaMemset(A, 1, (size_t)M * K);
-  cudaMemset(B, 1, (size_t)N * K);
+  if (rnd) {
+    bench_fill_kernel<<<1184, 256>>>(A, (size_t)M * K, 12345u);
+    bench_fill_kernel<<<1184, 256>>>(B, (size_t)N * K, 777u);
+  } else {
+    cudaMemset(A, 1, (size_t)M * K);
+    cudaMemset(B, 1, (size_t)N * K);
+  }
   float h_tab[QTAB_FLOATS];
   h_tab[0] = -INFINITY;
   for (int k = 1; k < 128; ++k) h_tab[k] = logf(expm1f((k - 0.5f) * 0.01f));  // ~softplus^-1 level bounds
