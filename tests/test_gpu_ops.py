@@ -203,6 +203,37 @@ def test_hadamard_quant_ties_clamps_and_nonfinite(cuda, oracle, n):
         hadamard_quantize(bad, 1.0, plan)
 
 
+@pytest.mark.parametrize("M,D", [(700, 2560), (1300, 768)])
+def test_rmsnorm_single_stream_bit_exact(cuda, oracle, M, D):
+    """The model's layers >= 1 (out_proj already accumulated into the stream) and its
+    final norm: rmsnorm of one stream -> int8 codes, or -> f32 (persistent kernel)."""
+    from paper_2410_13229_b200 import _device, _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(M)
+    x = (rng.standard_normal((M, D)) * 3).astype(np.float32)
+    x[1, ::3] = -0.0
+    x[2] *= np.float32(1e-20)
+    x[3, :5] = np.float32(3e-38)
+    x[4] *= np.float32(1e15)
+    x[5, :] = 0.0
+    gain = rng.uniform(0.5, 1.5, D).astype(np.float32)
+    xd, gd = torch.from_numpy(x).cuda(), torch.from_numpy(gain).cuda()
+    u = torch.empty((M, D), dtype=torch.int8, device="cuda")
+    y = torch.empty((M, D), dtype=torch.float32, device="cuda")
+    err = _device.err_flag()
+    st = _device.stream_ptr()
+    for s_out in (0.02, 0.005):
+        _lib.check(lib.qmb_rmsnorm_residual_quant(xd.data_ptr(), None, None, gd.data_ptr(), M, D, s_out, 8,
+                                                  u.data_ptr(), None, err.ptr, st), "rmsnorm")
+        err.raise_if_set()
+        assert np.array_equal(u.cpu().numpy(), oracle.quantize(oracle.rmsnorm(x, gain), s_out)), s_out
+    _lib.check(lib.qmb_rmsnorm_residual_quant(xd.data_ptr(), None, None, gd.data_ptr(), M, D, 1.0, 8, None,
+                                              y.data_ptr(), err.ptr, st), "rmsnorm")
+    err.raise_if_set()
+    assert _bits_equal(y.cpu().numpy(), oracle.rmsnorm(x, gain))
+
+
 @pytest.mark.parametrize("M,D", [(3, 8), (6, 16), (33, 64), (50, 768), (17, 2560), (9, 1000),
                                  (700, 2560), (640, 768), (1200, 64), (600, 1000)])
 def test_rmsnorm_residual_quant_bit_exact(cuda, oracle, M, D):
