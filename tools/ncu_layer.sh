@@ -4,7 +4,7 @@
 # usage: tools/ncu_layer.sh OUTDIR "regex1:skip1 regex2:skip2 ..."
 set -u
 OUT=${1:-gpurun_out/ncu}
-SPECS=${2:-"gemm_i8_tc_kernel:0 gemm_i8_tc_kernel:1 gemm_i8_tc_kernel:2 gemm_i8_tc_kernel:3 scan_p2:0 conv_silu_quant:0 hadamard:0 rmsnorm:0 bc_dequant:0"}
+SPECS=${2:-"gemm_i8_tc_kernel:0 gemm_i8_tc_kernel:1 gemm_i8_tc_kernel:2 gemm_i8_tc_kernel:3 scan_p2:0 conv_silu_quant:0 hadamard:0 rmsnorm:0 rmsnorm:1 bc_dequant:0"}
 mkdir -p "$OUT"
 for SPEC in $SPECS; do
   K=${SPEC%%:*}; IDX=${SPEC##*:}

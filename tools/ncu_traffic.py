@@ -9,7 +9,7 @@ from pathlib import Path
 
 STAGE = {"gemm_i8_tc_kernel_0": "in_proj", "gemm_i8_tc_kernel_1": "x_proj", "gemm_i8_tc_kernel_2": "dt_proj",
          "gemm_i8_tc_kernel_3": "out_proj", "scan_p2_0": "scan", "scan_c1_0": "scan", "conv_silu_quant_0": "conv",
-         "hadamard_0": "hadamard_quant", "rmsnorm_0": "rmsnorm", "bc_dequant_0": "bc_dequant"}
+         "hadamard_0": "hadamard_quant", "rmsnorm_0": "rmsnorm_residual_layer0", "rmsnorm_1": "rmsnorm_final", "bc_dequant_0": "bc_dequant"}
 
 
 def parse(path):
