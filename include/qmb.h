@@ -203,7 +203,8 @@ int qmb_hadamard_quantize(const float* y, long long M, int p, int m, const int8_
 
 /* Elementwise restated transcendentals (parity harness): fn 0 np.exp f32,
  * 1 glibc expf, 2 glibc log1pf, 3 softplus (np.logaddexp(x,0)), 4 silu,
- * 5 silu hot-path variant (must equal 4 everywhere). */
+ * 5 silu hot-path variant, 6 / 7 the packed (f32x2) silu of the in_proj
+ * epilogue, low / high half (5, 6, 7 must equal 4 everywhere). */
 int qmb_eval_math(int fn, const float* x, float* y, long long n, qmb_stream_t stream);
 
 /* Exhaustive check: fn_a and fn_b bit-identical on all 2^32 float inputs?

@@ -833,14 +833,14 @@ extern "C" int qmb_measure_i8_peak(int iters, double* tops) {
 }
 
 extern "C" int qmb_eval_math(int fn, const float* x, float* y, long long n, qmb_stream_t stream) {
-  if (fn < 0 || fn > 5) return fail(QMB_E_ARG, "unknown function %d", fn);
+  if (fn < 0 || fn > 7) return fail(QMB_E_ARG, "unknown function %d", fn);
   QMB_CUDA(eval_math(fn, x, y, n, (cudaStream_t)stream), "eval_math");
   return 0;
 }
 
 extern "C" int qmb_verify_math(int fn_a, int fn_b, unsigned long long* mismatches, uint32_t* first_bad,
                                qmb_stream_t stream) {
-  if (fn_a < 0 || fn_a > 5 || fn_b < 0 || fn_b > 5) return fail(QMB_E_ARG, "unknown function");
+  if (fn_a < 0 || fn_a > 7 || fn_b < 0 || fn_b > 7) return fail(QMB_E_ARG, "unknown function");
   QMB_CUDA(verify_math(fn_a, fn_b, mismatches, first_bad, (cudaStream_t)stream), "verify_math");
   return 0;
 }

@@ -120,14 +120,18 @@ __device__ __forceinline__ void epi_quant32_plain(const float (&v)[32], float s,
 // (bias, residual add, silu or quantize) and staged, so the per-kind code is a
 // few hundred instructions: with the x and z chunks of a tile interleaved, the
 // fully unrolled 32-wide paths did not fit the instruction cache together.
-__device__ __forceinline__ void epi_silu8(float (&v)[8], bool row_valid) {
+__device__ __forceinline__ void epi_silu8(float (&v)[8], bool row_valid, unsigned long long one2,
+                                          unsigned long long negz2) {
   uint32_t bad = 0;
   float y[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    y[j] = silu_core(v[j]);
-    bad |= silu_core_ok(v[j]) ? 0u : (1u << j);
+  for (int j = 0; j < 8; j += 2) {
+    const float2 r = unpack_f32x2(silu_core2(pack_f32x2(v[j], v[j + 1]), one2, negz2));
+    y[j] = r.x;
+    y[j + 1] = r.y;
   }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) bad |= silu_core_ok(v[j]) ? 0u : (1u << j);
   if (!row_valid) bad = 0;
   if (bad) {
 #pragma unroll
@@ -170,7 +174,7 @@ __device__ __forceinline__ void epi_chunk_sub8(const EpiParams& ep, const EpiSeg
         v[3] = __fadd_rn(v[3], o0.w), v[4] = __fadd_rn(v[4], o1.x), v[5] = __fadd_rn(v[5], o1.y);
         v[6] = __fadd_rn(v[6], o1.z), v[7] = __fadd_rn(v[7], o1.w);
       }
-      if (sg.kind == EPI_F32_SILU) epi_silu8(v, m < M);
+      if (sg.kind == EPI_F32_SILU) epi_silu8(v, m < M, ep.one2, ep.negz2);
       // 32 rows x 16 floats per half, 64B rows, SWIZZLE_64B: quad q of a row at q ^ ((row >> 1) & 3)
       float* hb = stg + (g >> 1) * 512;
       const int qa = (g & 1) * 2;
@@ -1175,6 +1179,8 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
   ep.spin = 0;  // (spinning waits measured no faster for decode-size GEMMs)
   ep.small_acc = (long long)Kp * 128 * 128 < (1LL << 22) ? 1 : 0;
   ep.qtab_bias = QTAB_BIAS;
+  ep.one2 = kOne2;
+  ep.negz2 = kNegZero2;
   for (int s = 0; s < ep.nseg; ++s) ep.seg[s].out_inv = 1.0f / ep.seg[s].out_div;  // RN f32 reciprocal
   const bool tc_ok = (lda % 16 == 0) && (ldb % 16 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)Bt % 16 == 0) &&
                      Kp > 0;

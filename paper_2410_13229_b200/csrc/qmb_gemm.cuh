@@ -115,6 +115,7 @@ struct EpiParams {
   int spin;        // pipeline waits spin (short, latency-bound GEMMs: decode) instead of sleeping
   int small_acc;   // |acc| < 2^22 (K < 256): accumulators convert with i2f_small (set by gemm_i8)
   uint32_t qtab_bias;  // QTAB_BIAS (set by gemm_i8)
+  unsigned long long one2, negz2;  // packed {1, 1} / {-0, -0} as run-time operands (set by gemm_i8)
   int splitk;      // > 1: split-K over K blocks; partial int32 sums stored per split
   int32_t* acc32;  // [splitk, M, N] int32 partials; a second kernel sums them and runs the epilogue
 };

@@ -34,7 +34,7 @@ def test_transcendentals_bit_exact(cuda, oracle, fn, name):
     assert same.all(), f"{name}: {np.count_nonzero(~same)} mismatches, e.g. x={x[~same][:5]}"
 
 
-@pytest.mark.parametrize("fa,fb", [(4, 5)])
+@pytest.mark.parametrize("fa,fb", [(4, 5), (4, 6), (4, 7)])
 def test_hot_path_math_exhaustive(cuda, fa, fb):
     """Hot-path restatements equal the reference restatement on ALL 2^32 inputs."""
     from paper_2410_13229_b200 import _device, _lib
