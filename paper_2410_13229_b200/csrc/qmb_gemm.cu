@@ -227,20 +227,21 @@ __device__ __forceinline__ void epi_chunk_sub8(const EpiParams& ep, const EpiSeg
 // 32 epilogue values -> 32 int8 (packed little-endian)
 template <bool SP>
 __device__ __forceinline__ void epi_quant32(const float (&v)[32], const EpiSeg& g, const float* qtab, int qmax,
-                                            uint32_t& err, uint32_t (&packed)[8], uint32_t qtab_bias) {
+                                            uint32_t& err, uint32_t (&packed)[8], uint32_t qtab_bias,
+                                            unsigned long long one2, unsigned long long negz2) {
   if constexpr (SP) {
     if (g.kind == EPI_SOFTPLUS_Q && qtab) {
       const float lo = qtab[QTAB_LO], hi = qtab[QTAB_HI], qmaxf = (float)qmax;
       const uint32_t tab_b = softplus_tab_bias(qtab, qtab_bias);
+      const unsigned long long sinv2 = pack_f32x2(g.out_inv, g.out_inv);
       float chk = 0.0f;  // NaN-sticky: becomes NaN iff some v is not finite
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
         uint32_t b[4];
+        softplus_quant_table_bits2(v[j], v[j + 1], tab_b, sinv2, qmaxf, one2, negz2, b[0], b[1]);
+        softplus_quant_table_bits2(v[j + 2], v[j + 3], tab_b, sinv2, qmaxf, one2, negz2, b[2], b[3]);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          b[t] = softplus_quant_table_bits(v[j + t], tab_b, g.out_inv, qmaxf);
-          chk = __fmaf_rn(v[j + t], 0.0f, chk);
-        }
+        for (int t = 0; t < 4; ++t) chk = __fmaf_rn(v[j + t], 0.0f, chk);
         packed[j / 4] = __byte_perm(__byte_perm(b[0], b[1], 0x40), __byte_perm(b[2], b[3], 0x40), 0x5410);
       }
       bool miss = !(chk == 0.0f);
@@ -615,7 +616,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             }
           } else {
             uint32_t packed[8];
-            epi_quant32<EPIW == 16>(v, sg, qtab, ep.qmax, err, packed, ep.qtab_bias);
+            epi_quant32<EPIW == 16>(v, sg, qtab, ep.qmax, err, packed, ep.qtab_bias, ep.one2, ep.negz2);
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
             // 32 rows x 32 B, SWIZZLE_32B: 16B chunk c of row r at chunk c ^ ((r >> 2) & 1)
@@ -678,7 +679,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
             for (int j = 0; j < 32; j += 4) o[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
           } else {
             uint32_t packed[8];
-            epi_quant32<EPIW == 16>(v, sg, qtab, ep.qmax, err, packed, ep.qtab_bias);
+            epi_quant32<EPIW == 16>(v, sg, qtab, ep.qmax, err, packed, ep.qtab_bias, ep.one2, ep.negz2);
             uint4* o = reinterpret_cast<uint4*>(static_cast<int8_t*>(sg.out) + m * sg.ld + oc);
             o[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
             o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);

@@ -73,6 +73,32 @@ __device__ __forceinline__ uint32_t softplus_quant_table_bits(float v, uint32_t 
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(tab_b + 4u * b));
   return b + (v >= t ? 1u : 0u);
 }
+// softplus_quant_table_bits on two values: the float ops as FFMA2s (each half rounded
+// like the scalar op, run-time 1.0 / -0.0 operands), the rest per half; bit-identical
+// per half to the scalar function the sweep verifies.
+__device__ __forceinline__ void softplus_quant_table_bits2(float v0, float v1, uint32_t tab_b,
+                                                           unsigned long long sinv2, float qmaxf,
+                                                           unsigned long long one2, unsigned long long negz2,
+                                                           uint32_t& b0, uint32_t& b1) {
+  const float2 a = unpack_f32x2(fma2_rn(pack_f32x2(v0, v1), 0x3FB8AA3B3FB8AA3Bull, negz2));  // v * log2(e)
+  float e0, e1, l0, l1, t0, t1;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(a.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(a.y));
+  const float2 den = unpack_f32x2(fma2_rn(pack_f32x2(e0, e1), one2, one2));  // 1 + e
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l0) : "f"(den.x));
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l1) : "f"(den.y));
+  const float2 sl = unpack_f32x2(fma2_rn(pack_f32x2(l0, l1), 0x3F3172183F317218ull, negz2));  // l * ln(2)
+  const float sp0 = v0 > 15.0f ? v0 : sl.x, sp1 = v1 > 15.0f ? v1 : sl.y;
+  const float2 y = unpack_f32x2(fma2_rn(pack_f32x2(sp0, sp1), sinv2, 0xBF000000BF000000ull));  // sp / s - 1/2
+  const float2 bb = unpack_f32x2(fma2_rn(
+      pack_f32x2(fminf(fmaxf(y.x, 0.0f), qmaxf), fminf(fmaxf(y.y, 0.0f), qmaxf)), one2, 0x4B4000004B400000ull));
+  b0 = __float_as_uint(bb.x);
+  b1 = __float_as_uint(bb.y);
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(t0) : "r"(tab_b + 4u * b0));
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(t1) : "r"(tab_b + 4u * b1));
+  b0 += v0 >= t0 ? 1u : 0u;
+  b1 += v1 >= t1 ? 1u : 0u;
+}
 __device__ __forceinline__ int softplus_quant_table(float v, const float* __restrict__ tab, float s_inv,
                                                     float qmaxf) {
   return (int)(softplus_quant_table_bits(v, softplus_tab_bias(tab), s_inv, qmaxf) - 0x4B400000u);
