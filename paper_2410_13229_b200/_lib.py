@@ -11,7 +11,8 @@ import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libqmb.so"
+# QMB_LIB: an alternative in-tree build of the same ABI (A/B timing of kernel variants, tools/ab_lib.sh)
+LIB_PATH = Path(os.environ["QMB_LIB"]) if os.environ.get("QMB_LIB") else PKG / "libqmb.so"
 
 c_i8p = ctypes.c_void_p
 c_vp = ctypes.c_void_p
