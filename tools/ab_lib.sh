@@ -10,4 +10,5 @@ for i in 1 2 3; do
   echo "== B $i" >> gpurun_out/ab_lib.log
   QMB_LIB=$B timeout 300 python tools/profile_layer.py 2>&1 | tail -1 >> gpurun_out/ab_lib.log
 done
-if [ -n "$1" ]; then QMB_LIB=$B timeout 900 python -m pytest tests -m gpu -x -q $1 > gpurun_out/pytest_b.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_b.log; fi
+# optional: GPU tests of build B, "$1" = a pytest -k expression
+if [ -n "$1" ]; then QMB_LIB=$B timeout 900 python -m pytest tests -m gpu -x -q -k "$1" > gpurun_out/pytest_b.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_b.log; fi
