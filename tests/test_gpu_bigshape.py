@@ -1,0 +1,175 @@
+"""GPU parity at the BENCHMARKED kernel instantiations.
+
+The 2.8B-shape headline runs M = 65,536 rows per layer, where in_proj, dt_proj
+and out_proj take the CTA-pair tcgen05 GEMM (`gemm_i8_tc_kernel<256, W, 1, 2>`,
+chosen once ceil(M/256) * ceil(N/256) >= 74, qmb_gemm.cu gemm_i8).  The golden
+fixtures stop at M <= 16, so these tests drive the 2.8B block at M = 2048
+(B = 8 x T = 256: 8 x 40 in_proj, 8 x 20 dt_proj and 8 x 10 out_proj pair
+tiles) and compare every workspace stage, the output, the final scan state and
+the conv window with the oracle's stage replay of block_forward_q
+(qblock.py:185-215), sequence by sequence.  The launch list of this file
+(tools/parity_launches.sh) is the evidence that the pair kernels ran.
+"""
+import numpy as np
+import pytest
+import torch
+
+from fixtures_util import block_weights, load_block, mirror_block, oracle_block
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint32) if a.dtype == np.float32 else a
+
+
+def _stage_views(dev, ws, M, E, N, R):
+    lay = dev.workspace_layout(M)
+    Ep = (E + 15) // 16 * 16
+    Rp = (R + 15) // 16 * 16
+
+    def view(slot, dtype, cols, ld):
+        nb = torch.tensor([], dtype=dtype).element_size()
+        return ws[lay[slot]:lay[slot] + M * ld * nb].view(dtype).reshape(M, ld)[:, :cols].cpu().numpy()
+
+    return {"x_q": view("XQ", torch.int8, E, E), "scan_x": view("SCANX", torch.int8, E, Ep),
+            "b_q": view("B", torch.int8, N, N), "c_q": view("C", torch.int8, N, N),
+            "dtr_q": view("DTR", torch.int8, R, Rp), "delta_q": view("DELTA", torch.int8, E, E),
+            "gated": view("Z", torch.float32, E, E), "y_q": view("YQ", torch.int8, E, Ep)}
+
+
+@pytest.fixture(scope="module")
+def s2p8b():
+    z, meta = load_block("s2p8b")
+    w = block_weights(z, meta)
+    return z, meta, mirror_block(z, meta, w), oracle_block(z, meta, w)
+
+
+@pytest.fixture(scope="module")
+def s2p8b_run(s2p8b, oracle):
+    """One B=8 x T=256 prefill of the 2.8B block + the oracle's per-sequence replay."""
+    import paper_2410_13229_b200  # noqa: F401
+    from paper_2410_13229_b200 import _device
+    from paper_2410_13229_b200.qblock import device_block
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    z, meta, qb, ob = s2p8b
+    c = meta["cfg"]
+    D, E, N, R = c["d_model"], c["d_inner"], c["d_state"], c["dt_rank"]
+    B, T = 8, 256
+    rng = np.random.default_rng(2048)
+    u = rng.integers(-127, 128, size=(B, T, D)).astype(np.int8)
+    dev = device_block(qb)
+    M = B * T
+    ws = torch.zeros(dev.workspace_bytes(M), dtype=torch.uint8, device="cuda")
+    out = torch.empty((M, D), dtype=torch.float32, device="cuda")
+    conv, h = dev.new_state(B)
+    ud = torch.from_numpy(u).cuda().reshape(M, D)
+    dev.prefill(ud, B, T, out, u_scale=meta["u_scale"], conv_state_out=conv, ssm_state_out=h, workspace=ws)
+    _device.err_flag().raise_if_set()
+    views = _stage_views(dev, ws, M, E, N, R)
+    # accumulate variant (out_proj EPI_F32_ADDTO pair epilogue): res += block output
+    res0 = rng.standard_normal((M, D)).astype(np.float32)
+    res = torch.from_numpy(res0).cuda()
+    dev.prefill(ud, B, T, res, u_scale=meta["u_scale"], accumulate=True, workspace=ws)
+    _device.err_flag().raise_if_set()
+    ref = [oracle.block_stages(u[b], meta["u_scale"], ob) for b in range(B)]
+    return dict(B=B, T=T, out=out.cpu().numpy().reshape(B, T, D), conv=conv.cpu().numpy(), h=h.cpu().numpy(),
+                views={k: v.reshape(B, T, -1) for k, v in views.items()}, res=res.cpu().numpy(), res0=res0, ref=ref)
+
+
+@pytest.mark.parametrize("stage", ["x_q", "scan_x", "b_q", "c_q", "dtr_q", "delta_q", "gated", "y_q"])
+def test_2p8b_pair_gemm_stage_bit_exact(cuda, s2p8b_run, stage):
+    """in_proj <256,12,1,2> (int8 x | silu(z)), x_proj, dt_proj <256,16,1,2>
+    (softplus-quantize), scan, Hadamard at M = 2048."""
+    r = s2p8b_run
+    for b in range(r["B"]):
+        got, ref = r["views"][stage][b], r["ref"][b][stage]
+        assert np.array_equal(_bits(got), _bits(ref)), \
+            f"seq {b} stage {stage}: {np.count_nonzero(_bits(got) != _bits(ref))} of {ref.size} differ"
+
+
+def test_2p8b_pair_gemm_out_state_bit_exact(cuda, s2p8b_run):
+    """out_proj <256,8,1,2> f32 output, final scan state h, conv window."""
+    r = s2p8b_run
+    for b in range(r["B"]):
+        st = r["ref"][b]
+        assert np.array_equal(_bits(r["out"][b]), _bits(st["out"])), b
+        assert np.array_equal(_bits(r["h"][b]), _bits(st["h"])), b
+        assert np.array_equal(r["conv"][b], st["conv_state"]), b
+
+
+def test_2p8b_pair_gemm_accumulate_bit_exact(cuda, s2p8b_run):
+    """out_proj's pair EPI_F32_ADDTO epilogue == the f32 residual add of
+    fused_rmsnorm_quant (qblock.py:181)."""
+    r = s2p8b_run
+    ref = np.concatenate([st["out"] for st in r["ref"]]) + r["res0"]
+    assert np.array_equal(_bits(r["res"]), _bits(ref))
+
+
+@pytest.mark.parametrize("M,K,N,quant", [(4096, 2560, 10240, True), (4096, 2560, 10240, False),
+                                         (2304, 5120, 2560, True), (1024, 160, 5120, True)])
+def test_qlinear_pair_aligned_bit_exact(cuda, oracle, M, K, N, quant):
+    """qlinear at 16-byte-aligned int8 N: the pair kernel's TMA-store SUB8
+    EPI_QUANT path (and f32) -- qblock.py:98-123."""
+    from paper_2410_13229_b200 import QTensor, qlinear
+
+    rng = np.random.default_rng(M + N + K)
+    x = rng.integers(-127, 128, size=(M, K)).astype(np.int8)
+    w = rng.integers(-127, 128, size=(K, N)).astype(np.int8)
+    bias = rng.integers(-127, 128, size=(N,)).astype(np.int8)
+    sx, sw, sb = 0.013, 0.0021, 0.05
+    s_out = 0.9 if quant else None
+    got = qlinear(QTensor(torch.from_numpy(x).cuda(), sx), QTensor(torch.from_numpy(w).cuda(), sw),
+                  QTensor(torch.from_numpy(bias).cuda(), sb), s_out=s_out)
+    ref = oracle.qlinear(x, sx, w, sw, (bias, sb), s_out=s_out)
+    g = (got.values if quant else got).cpu().numpy()
+    assert np.array_equal(_bits(g), _bits(ref)), np.count_nonzero(_bits(g) != _bits(ref))
+
+
+def test_130m_two_layer_model_hidden_bit_exact(cuda, oracle):
+    """A 2-layer 130M-shape model (D=768, E=1536, m=12 Hadamard), synthetic
+    weights + scales, B=2 x T=1024: the final hidden state is bit-exact with
+    the oracle's forward_q replay (model.py:246-257); M = 2048 puts in_proj on
+    the CTA-pair kernel (8 x 12 pair tiles)."""
+    from oracle import oracle as o
+    from paper_2410_13229_b200.model import ModelConfig, device_model
+    from paper_2410_13229_b200.synthetic import build_model
+
+    cfg = ModelConfig(vocab_size=50280, d_model=768, n_layers=2, d_state=16, dt_rank=48)
+    qm = build_model(cfg, seed=3, calib_tokens=256)
+    om = o.Model.from_object(_host_model(qm))
+    rng = np.random.default_rng(7)
+    toks = rng.integers(0, cfg.vocab_size, size=(2, 1024))
+    dm = device_model(qm)
+    hid = dm.forward_hidden(torch.from_numpy(toks).cuda()).cpu().numpy().reshape(2, 1024, cfg.d_model)
+    for b in range(2):
+        ref = o.forward_hidden(om, toks[b])
+        assert np.array_equal(_bits(hid[b]), _bits(ref)), (b, np.count_nonzero(_bits(hid[b]) != _bits(ref)))
+
+
+def _host_model(qm):
+    """A host (numpy) copy of a device-built QuantizedModel for the oracle."""
+    import copy
+
+    from paper_2410_13229_b200.quant import QTensor
+
+    def host(v):
+        return v.detach().cpu().numpy() if isinstance(v, torch.Tensor) else v
+
+    h = copy.copy(qm)
+    h.embedding = host(qm.embedding)
+    h.final_norm = host(qm.final_norm)
+    layers = []
+    for layer in qm.layers:
+        l2 = copy.copy(layer)
+        l2.norm_weight = host(layer.norm_weight)
+        b2 = copy.copy(layer.block)
+        b2.__dict__.pop("_qmb_device", None)
+        b2.weights = {k: QTensor(host(v.values), v.scale, v.zero_point, v.bit_width) for k, v in layer.block.weights.items()}
+        l2.block = b2
+        layers.append(l2)
+    h.layers = layers
+    return h
