@@ -7,12 +7,15 @@ block, final norm, last-position tied LM head, greedy argmax) on device-resident
 inputs.  `e2e` is the same step through the public API with the tokens copied
 from pinned host memory and the last-position logits copied back.  Decode
 (carried state, one token per sequence) is measured after it.
-Reference arm (--impl reference): the CPU oracle port of the reference's
-algorithm (oracle/) on the host cores, bounded sample, extrapolated.
+Reference arm (--impl reference): the reference itself (ssmq with its compiled
+Cython backend, built into oracle/_ref by oracle/build_ref.sh) timed on all
+host cores, one 2.8B layer per process on a bounded token sample, extrapolated
+linearly to 64 layers; the oracle port stands in only if oracle/_ref is absent.
 
-Multi-GPU: one process per GPU (torchrun); sequences are batch-sharded (weak
-scaling: B per GPU); the only collective is an all_gather of the generated
-token ids (NCCL over NVLink).
+Multi-GPU: one process per GPU; `--gpus N` starts the N ranks itself
+(torch.distributed.run) unless already under torchrun; sequences are
+batch-sharded (weak scaling: B per GPU); the only collective is an all_gather
+of the generated token ids (NCCL over NVLink).
 """
 from __future__ import annotations
 
@@ -96,9 +99,53 @@ def _dist_env():
 
 
 # ============================================================== CPU reference arm
+REF_DIR = ROOT / "oracle" / "_ref"   # the real reference, built by oracle/build_ref.sh (git-ignored)
+SHAPE_2P8B = dict(d_model=2560, d_inner=5120, d_state=16, d_conv=4, dt_rank=160)
+
+
+def _have_ref() -> bool:
+    return (REF_DIR / "ssmq").is_dir()
+
+
+def _ref_layer_sample(args):
+    """Time one 2.8B-shape layer of the UNMODIFIED reference (ssmq, compiled
+    Cython backend): fused_rmsnorm_quant (qblock.py:170) + block_forward_q
+    (qblock.py:185) on T tokens, exactly the per-layer body of forward_q
+    (model.py:251-256).  Returns seconds.  Weights follow the reference's own
+    init + quantize_block (ssm.py:183-210, qblock.py:223-240)."""
+    T, seed = args
+    import sys as _s
+    _s.path.insert(0, str(REF_DIR))
+    import numpy as np
+    import ssmq.hadamard as rh
+    from ssmq import kernels
+    from ssmq.qblock import ACT_SITES, Mode, ScaleEntry, block_forward_q, fused_rmsnorm_quant, quantize_block
+    from ssmq.quant import QuantScheme, SchemeKind
+    from ssmq.ssm import BlockConfig, init_block_params
+
+    assert kernels.backend_name() == "compiled"
+    rh.MAX_TRANSFORM_DIM = 8192  # SURVEY §8c: the 2.8B shape needs the patched transform bound
+    c = SHAPE_2P8B
+    cfg = BlockConfig(d_model=c["d_model"], expand=2, d_state=c["d_state"], d_conv=c["d_conv"], dt_rank=c["dt_rank"])
+    rng = np.random.default_rng(seed)
+    params = init_block_params(cfg, rng)
+    sch = QuantScheme(SchemeKind.STATIC_SYMMETRIC_MAX)
+    scales = {"in": 0.03, "conv_in": 0.02, "conv_out": 0.01, "x": 0.01, "b": 0.01, "c": 0.01, "dt_r": 0.01,
+              "dt": 0.1 / 127, "y": 0.01, "y_had": 0.2}
+    act = {k: ScaleEntry(scales[k], 0, sch) for k in ACT_SITES}
+    act["x"] = ScaleEntry(scales["x"], 0, QuantScheme(SchemeKind.STATIC_SYMMETRIC_PERCENTILE, 99.999))
+    blk = quantize_block(params, cfg, act, Mode.FULL, rh.plan_for_dim(cfg.d_inner))
+    x = rng.standard_normal((T, c["d_model"])).astype(np.float32)
+    gain = np.ones(c["d_model"], np.float32)
+    t0 = time.perf_counter()
+    u_q, res = fused_rmsnorm_quant(x, np.zeros_like(x), gain, 0.03)
+    block_forward_q(u_q, blk)
+    return time.perf_counter() - t0
+
+
 def _oracle_layer_sample(args):
-    """Time one 2.8B-shape layer (fused_rmsnorm_quant + block_forward_q) of the CPU
-    oracle port on T tokens; returns seconds."""
+    """Fallback when the reference was not built: the CPU oracle port (oracle/),
+    same per-layer work.  Returns seconds."""
     T, seed = args
     import numpy as np
     from oracle import oracle as o
@@ -127,57 +174,139 @@ def _oracle_layer_sample(args):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(T: int = 8, procs: int = 1, layers: int = 64):
-    """Oracle port (kind "port"): per-layer sample on `procs` processes, linear
-    extrapolation in layers (SURVEY.md §8d verified linearity in T and L)."""
-    if procs <= 1:
-        secs = [_oracle_layer_sample((T, 0))]
+def cpu_baseline(T: int = 8, procs: int = 1, layers: int = 64, pool=None):
+    """The reference's CPU path on the host: the real ssmq when oracle/_ref was
+    built (kind "reference"), else the oracle port (kind "port").  One 2.8B
+    layer at T tokens per process (`procs` independent sequences in parallel,
+    SPEC.md:393), extrapolated linearly x layers (linear in T, L)."""
+    ref = _have_ref()
+    fn = _ref_layer_sample if ref else _oracle_layer_sample
+    if pool is None:
+        secs = [fn((T, 0))]
+        procs = 1
     else:
-        from multiprocessing import get_context
-        with get_context("spawn").Pool(procs) as pool:
-            secs = pool.map(_oracle_layer_sample, [(T, i) for i in range(procs)])
+        secs = pool.map(fn, [(T, i) for i in range(procs)])
     t = max(secs)
     value = procs * T / (t * layers)
-    return {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+    what = ("ssmq (the reference, compiled Cython backend, oracle/_ref) fused_rmsnorm_quant + block_forward_q"
+            if ref else "oracle/ CPU restatement (numpy int32 matmul via f64 BLAS + C scan)")
+    return {"value": value, "unit": UNIT, "cores": procs, "kind": "reference" if ref else "port",
             "sample": f"{procs} process(es) x 1 layer of the 2.8B shape (D=2560,E=5120,N=16,R=160) at T={T} "
-                      f"tokens, {t:.2f} s/layer, extrapolated x{layers} layers (oracle/ CPU restatement, "
-                      f"numpy int32 matmul + C scan)"}
+                      f"tokens each, {t:.2f} s/layer, extrapolated x{layers} layers; {what}"}
 
 
 def run_reference(args):
     rank, world, _ = _dist_env()
     if rank != 0:
         return
+    from multiprocessing import get_context
+
     procs = max(1, (os.cpu_count() or 1))
-    T = 8
-    import oracle.oracle as _o  # warm-up: build/load the C oracle and numpy before timing
-    _o.lib()
-    t0 = time.perf_counter()
-    vals = []
-    for _ in range(args.steps):
-        vals.append(cpu_baseline(T=T, procs=procs)["value"])
-    elapsed = time.perf_counter() - t0
+    T = args.ref_tokens
+    with get_context("spawn").Pool(procs) as pool:
+        for _ in range(min(args.warmup, 1)):  # imports + first-touch outside the timed samples
+            cpu_baseline(T=1, procs=procs, pool=pool)
+        t0 = time.perf_counter()
+        vals = []
+        cb = None
+        for _ in range(args.steps):
+            cb = cpu_baseline(T=T, procs=procs, pool=pool)
+            vals.append(cb["value"])
+        elapsed = time.perf_counter() - t0
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / max(args.steps, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int8/int32/f32", "data": "synthetic",
-            "config": {"workload": "2.8B-shape W8A8 prefill, CPU oracle port sample", "d_model": 2560,
-                       "n_layers": 64, "d_state": 16, "dt_rank": 160, "tokens_per_layer_sample": T},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": procs, "kind": "port",
-                             "sample": f"{procs} processes x 1 layer x T={T}, extrapolated x64 layers"},
+            "config": {"workload": f"Mamba-2.8b-shape W8A8 prefill (reference CPU path, bounded sample)",
+                       "d_model": 2560, "n_layers": 64, "d_state": 16, "dt_rank": 160,
+                       "tokens_per_layer_sample": T, "same_config": False},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": procs, "kind": cb["kind"], "sample": cb["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ============================================================== GPU arm
+def _timed(fn, n, stream, world, dev):
+    """CUDA-event time of n calls on `stream` (barrier + synchronize on both
+    sides), max over ranks.  Returns ms per call."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / n
+    if world > 1:
+        t = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def _decode_bytes(cfg, B: int) -> float:
+    """Algorithmic HBM bytes of one decode step: every int8 weight
+    once, the f32 state h read + written and the int8 conv window read +
+    written per sequence and layer, the f32 tied embedding once (LM head)."""
+    D, E, N, K, R, L, V = cfg.d_model, cfg.d_inner, cfg.d_state, cfg.d_conv, cfg.dt_rank, cfg.n_layers, cfg.vocab_size
+    w = D * 2 * E + E * (2 * N + R) + R * E + E * D + K * E + E * N + 3 * E
+    state = B * (E * N * 4 * 2 + (K - 1) * E * 2)
+    return float(L * (w + state) + V * D * 4)
+
+
+def _decode_line(dm, cfg, tokens, B, steps, stream, world, dev, hbm):
+    """Decode with carried state: prefill 16 tokens, capture one CUDA graph of a
+    full decode step (all layers + LM head), time its replay."""
+    _, states = dm.prefill(tokens[:B, :16].contiguous())
+    graph, tok_in, _ = dm.capture_decode(states)
+    tok_in.copy_(tokens[:B, 0])
+    for _ in range(3):
+        graph.replay()
+    ms = _timed(graph.replay, steps, stream, world, dev)
+    nbytes = _decode_bytes(cfg, B)
+    ach = nbytes / (ms * 1e-3) / 1e9
+    del graph, states
+    return {"value": world * B / (ms * 1e-3), "unit": "tokens/s", "batch_per_gpu": B, "ms_per_token": ms,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                         "algorithmic_bytes_per_step": nbytes},
+            "note": "one token per sequence per step, carried (conv window, h) state, CUDA-graph replay"}
+
+
+def _prefill_line(dm, tokens, steps, stream, world, dev):
+    B, T = tokens.shape
+    dm.forward(tokens, last_only=True)
+    ms = _timed(lambda: dm.forward(tokens, last_only=True), steps, stream, world, dev)
+    return {"value": world * B * T / (ms * 1e-3), "unit": "tokens/s", "batch_per_gpu": B, "seq_len": T,
+            "ms_per_step": ms}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     rank, world, local = _dist_env()
-    torch.cuda.set_device(local)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch through torchrun or let "
+                         f"bench.py spawn the ranks)")
+    ndev = torch.cuda.device_count()
+    shared = False
+    if ndev < world:
+        if not args.shared_gpu_dry_run:
+            raise SystemExit(f"bench.py: --gpus {world} needs {world} GPUs, this node has {ndev}")
+        shared = True  # plumbing dry run: ranks share the GPU(s); NCCL refuses that, so gloo
+    torch.cuda.set_device(local % max(ndev, 1))
+    backend = None
     if world > 1:
-        dist.init_process_group("nccl")
+        backend = "gloo" if shared else "nccl"
+        dist.init_process_group(backend)
+        assert dist.get_world_size() == world
     from paper_2410_13229_b200 import _device, _lib
     from paper_2410_13229_b200.model import device_model
     from paper_2410_13229_b200.synthetic import CONFIGS, build_model
@@ -195,6 +324,8 @@ def run_ours(args):
     gen.manual_seed(1234 + rank)
     tokens = torch.randint(0, cfg.vocab_size, (B, T), device=dev, generator=gen)
     stream = torch.cuda.current_stream()
+    peaks = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
 
     gathered = torch.empty((world * B,), dtype=torch.int64, device=dev)
 
@@ -202,7 +333,11 @@ def run_ours(args):
         logits = dm.forward(tok, last_only=True)
         nxt = torch.argmax(logits, dim=-1)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, nxt)
+            if shared:  # gloo dry run: host copies
+                parts = [torch.empty_like(nxt, device="cpu") for _ in range(world)]
+                dist.all_gather(parts, nxt.cpu())
+            else:
+                dist.all_gather_into_tensor(gathered, nxt)
         return logits, nxt
 
     for _ in range(args.warmup):
@@ -218,27 +353,8 @@ def run_ours(args):
         print(json.dumps({"ncu_step": "done", "config": args.config, "batch": B, "seq": T}), flush=True)
         return
 
-    def timed(fn, n):
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(n):
-            fn()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        ms = e0.elapsed_time(e1) / n
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
-
-    with ClockSampler(local) as clk:
-        ms = timed(lambda: step(tokens), args.steps)
+    with ClockSampler(local % max(ndev, 1)) as clk:
+        ms = _timed(lambda: step(tokens), args.steps, stream, world, dev)
     value = world * B * T / (ms * 1e-3)
 
     # ---------------------------------------------------------- e2e through the public API
@@ -252,19 +368,23 @@ def run_ours(args):
         host_logits.copy_(logits, non_blocking=True)
 
     e2e_step()
-    ms_e2e = timed(e2e_step, max(1, args.steps))
+    ms_e2e = _timed(e2e_step, max(1, args.steps), stream, world, dev)
     e2e = {"value": world * B * T / (ms_e2e * 1e-3), "unit": UNIT,
            "h2d_bytes_per_step": host_tok.numel() * 8, "d2h_bytes_per_step": host_logits.numel() * 4}
 
-    # ---------------------------------------------------------- decode (carried state)
-    _, states = dm.prefill(tokens[:, :16])
-    graph, tok_in, _ = dm.capture_decode(states)  # one CUDA graph per decode step (all 64 layers)
-    tok_in.copy_(tokens[:, 0])
-    for _ in range(3):
-        graph.replay()
-    ms_dec = timed(graph.replay, max(10, args.steps * 8))
-    decode = {"value": world * B / (ms_dec * 1e-3), "unit": "tokens/s", "batch_per_gpu": B, "ms_per_token": ms_dec,
-              "note": "one token per sequence per step, carried (conv window, h) state, CUDA-graph replay"}
+    # ---------------------------------------------------------- decode (carried state), B and 1
+    decode = _decode_line(dm, cfg, tokens, B, max(10, args.steps * 8), stream, world, dev, hbm)
+    extras = {}
+    if not args.no_extras:
+        # BASELINE config 3, batch 1: prefill 1K tokens of one sequence + decode at B = 1
+        extras["batch1_prefill"] = _prefill_line(dm, tokens[:1].contiguous(), max(3, args.steps), stream, world, dev)
+        extras["batch1_decode"] = _decode_line(dm, cfg, tokens, 1, max(20, args.steps * 8), stream, world, dev, hbm)
+        # BASELINE config 4 per-GPU shard: 32 sequences x 16K tokens over 8 GPUs = 4 x 16K per GPU
+        Tl = 16384
+        ltok = torch.randint(0, cfg.vocab_size, (4, Tl), device=dev, generator=gen)
+        extras["long_context_4x16k"] = _prefill_line(dm, ltok, 2, stream, world, dev)
+        del ltok
+        torch.cuda.empty_cache()
 
     # ---------------------------------------------------------- roofline of the dominant kernel
     import ctypes
@@ -282,18 +402,18 @@ def run_ours(args):
                                                   stream.cuda_stream, stage_ms))
         if r:
             acc = [a + s / reps for a, s in zip(acc, stage_ms)]
+    del u, out
     names = ["in_proj", "conv", "x_proj", "dt_proj", "scan", "hadamard_quant", "out_proj"]
     D, E, N, R = cfg.d_model, cfg.d_inner, cfg.d_state, cfg.dt_rank
     peak_i8 = ctypes.c_double()
     _lib.check(lib.qmb_measure_i8_peak(2000, ctypes.byref(peak_i8)))
-    peaks = _peaks()
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
-    # algorithmic work per launch
+    # algorithmic work per launch.  x_proj / dt_proj are skinny GEMMs whose
+    # binding roofline is HBM: activation bytes in + out.
     work = {
         "in_proj": ("tensor", 2.0 * M * D * 2 * E / 1e12, "TFLOP/s"),
         "out_proj": ("tensor", 2.0 * M * E * D / 1e12, "TFLOP/s"),
-        "x_proj": ("tensor", 2.0 * M * E * (2 * N + R) / 1e12, "TFLOP/s"),
-        "dt_proj": ("tensor", 2.0 * M * R * E / 1e12, "TFLOP/s"),
+        "x_proj": ("hbm", (M * E + M * (2 * N + R) + E * (2 * N + R)) / 1e9, "GB/s"),
+        "dt_proj": ("hbm", (M * R + M * E + R * E) / 1e9, "GB/s"),
         "conv": ("hbm", M * E * 2 / 1e9, "GB/s"),
         "scan": ("hbm", M * E * (1 + 1 + 4 + 4) / 1e9 + M * 2 * N / 1e9, "GB/s"),
         "hadamard_quant": ("hbm", M * E * 5 / 1e9, "GB/s"),
@@ -324,7 +444,19 @@ def run_ours(args):
                                 else "MEASURED_PEAKS.json hbm_gbs"),
                 "per_kernel": per}
 
-    cpu = cpu_baseline(T=8, procs=1) if (rank == 0 and world == 1 and not args.no_cpu) else None
+    # ---------------------------------------------------------- BASELINE config 2: 130M shape
+    if not args.no_extras and args.config == "2.8b":
+        del dm, qm
+        torch.cuda.empty_cache()
+        c130 = CONFIGS["130m"]
+        qm130 = build_model(c130, seed=args.seed, calib_tokens=args.calib_tokens)
+        dm130 = device_model(qm130)
+        tok130 = torch.randint(0, c130.vocab_size, (1, 2048), device=dev, generator=gen)
+        extras["130m_prefill_2k"] = _prefill_line(dm130, tok130, max(3, args.steps), stream, world, dev)
+        extras["130m_decode_b1"] = _decode_line(dm130, c130, tok130, 1, 128, stream, world, dev, hbm)
+        extras["130m_decode_b1"]["note"] = "128 greedy-decode-shaped steps at batch 1 (CUDA-graph replay)"
+
+    cpu = cpu_baseline(T=8) if (rank == 0 and world == 1 and not args.no_cpu) else None
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -337,7 +469,9 @@ def run_ours(args):
                            "parallelism": f"dp{world} (batch-sharded, all_gather of next tokens)",
                            "l2": "inputs larger than L2 (per-layer activations >= 1.3 GB)",
                            "step": "embed + 64x(rmsnorm+block) + final norm + last-position LM head + argmax"},
-                "e2e": e2e, "decode": decode, "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "decode": decode, "extras": extras, "roofline": roofline, "cpu_baseline": cpu,
+                "comm": {"backend": backend, "world_size": world,
+                         "dry_run_shared_gpu": shared, "collective": "all_gather_into_tensor of next-token ids"},
                 # ours per step: embed + 64 x (rmsnorm, in_proj, conv, x_proj, dt_proj, bc_dequant, scan,
                 # hadamard, out_proj) + final norm (the cuBLAS LM head and torch argmax are not counted)
                 "clocks": clk.summary(), "gpu_launches": 2 + 9 * cfg.n_layers,
@@ -345,6 +479,19 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _spawn_ranks(args) -> int:
+    """--gpus N > 1 outside torchrun: start N ranks (one process per GPU) with
+    torch.distributed.run on 127.0.0.1 and return its exit code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -358,9 +505,15 @@ def main():
     ap.add_argument("--seq", type=int, default=1024)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--calib-tokens", type=int, default=256)
+    ap.add_argument("--ref-tokens", type=int, default=8, help="reference arm: tokens per layer sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip batch-1 / long-context / 130M lines")
+    ap.add_argument("--shared-gpu-dry-run", action="store_true",
+                    help="let N ranks share fewer GPUs (gloo) to exercise the multi-rank path; not a measurement")
     ap.add_argument("--ncu", action="store_true", help="profile one prefill step (ncu --profile-from-start off)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     else:
