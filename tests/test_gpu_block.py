@@ -123,6 +123,38 @@ def test_block_many_sequences_bit_exact(cuda, oracle, name, B, T):
         assert np.array_equal(hs[b].view(np.uint32), st["h"].view(np.uint32)), b
 
 
+@pytest.mark.parametrize("name,B,T", [("m12_full", 1, 1), ("m12_full", 2, 2), ("m20_full", 3, 3), ("m20_full", 5, 47),
+                                      ("m20_full", 2, 1000), ("p2_naive", 4, 16), ("p2_inper", 7, 33),
+                                      ("s130m", 1, 100), ("s130m", 15, 21), ("s2p8b", 2, 40), ("s2p8b", 4, 17)])
+def test_block_small_batch_bit_exact(cuda, oracle, name, B, T):
+    """B < 16 takes the state-split scan (4 lanes per channel, skewed one step
+    apart, the in-order acc sum handed lane to lane): ragged T (shorter than the
+    skew, not a multiple of the 16-step chunk, 1000 steps) and partial
+    sequence groups; outputs and final states bit-exact against the oracle."""
+    from paper_2410_13229_b200 import _device
+    from paper_2410_13229_b200.qblock import device_block
+
+    z, meta = load_block(name)
+    w = block_weights(z, meta)
+    qb = mirror_block(z, meta, w)
+    ob = oracle_block(z, meta, w)
+    dev = device_block(qb)
+    D = meta["cfg"]["d_model"]
+    rng = np.random.default_rng(B * 1000 + T)
+    u = rng.integers(-127, 128, size=(B, T, D)).astype(np.int8)
+    out = torch.empty((B * T, D), dtype=torch.float32, device="cuda")
+    conv, h = dev.new_state(B)
+    dev.prefill(torch.from_numpy(u).cuda().reshape(B * T, D), B, T, out, u_scale=meta["u_scale"],
+                conv_state_out=conv, ssm_state_out=h)
+    _device.err_flag().raise_if_set()
+    got = out.reshape(B, T, D).cpu().numpy()
+    hs = h.cpu().numpy()
+    for b in range(B):
+        st = oracle.block_stages(u[b], meta["u_scale"], ob)
+        assert np.array_equal(got[b].view(np.uint32), st["out"].view(np.uint32)), b
+        assert np.array_equal(hs[b].view(np.uint32), st["h"].view(np.uint32)), b
+
+
 @pytest.mark.parametrize("name", ["tiny_full", "m12_full", "p2_inper", "s2p8b"])
 def test_block_decode_equals_prefill(cuda, name):
     """Prefill k tokens (exporting state), then decode the rest one by one: every
