@@ -193,7 +193,10 @@ int qmb_selective_scan(const int8_t* a_q, double s_a, const int8_t* b_q, double 
                        const int8_t* c_q, double s_c, const int8_t* d_q, double s_d,
                        const int8_t* dt_q, double s_dt, const int8_t* x_q, double s_x,
                        int B, int T, int D, int N, float* h, int h_in, float* y,
-                       uint32_t* err_flag, qmb_stream_t stream);
+                       void* ws, size_t ws_bytes, uint32_t* err_flag, qmb_stream_t stream);
+/* Device workspace qmb_selective_scan needs for d_inner D, d_state N (its
+ * dequantized a / d and dequant tables; the library allocates nothing per call). */
+size_t qmb_selective_scan_workspace_bytes(int D, int N);
 
 /* hadamard_quantize (hadamard.py:164-166): y [M, n] f32, n = 2^p*m ->
  * out [M, n] int8; y_h (nullable) receives the f32 transform (apply_hadamard). */

@@ -68,7 +68,8 @@ PROTOTYPES = {
     "qmb_fused_qconv": (c_int, [c_i8p, c_int, c_int, c_int, c_dbl, c_i8p, c_int, c_dbl, c_i8p, c_dbl, c_dbl, c_int,
                                 c_i8p, c_vp, c_vp]),
     "qmb_selective_scan": (c_int, [c_i8p, c_dbl, c_i8p, c_dbl, c_i8p, c_dbl, c_i8p, c_dbl, c_i8p, c_dbl, c_i8p,
-                                   c_dbl, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_vp, c_vp]),
+                                   c_dbl, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_vp, c_sz, c_vp, c_vp]),
+    "qmb_selective_scan_workspace_bytes": (c_sz, [c_int, c_int]),
     "qmb_hadamard_quantize": (c_int, [c_vp, c_ll, c_int, c_int, c_i8p, c_dbl, c_int, c_i8p, c_vp, c_vp, c_vp]),
     "qmb_measure_i8_peak": (c_int, [c_int, ctypes.POINTER(c_dbl)]),
     "qmb_gemm_bench": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(ctypes.c_float)]),

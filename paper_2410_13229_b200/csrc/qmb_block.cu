@@ -89,6 +89,7 @@ struct qmb_block {
   int8_t* w_out_t;  // [D, Ep]
   float* luts;      // [4][256] dequant tables: x, dt, b, c (index q + 128)
   float* sp_qtab;   // [QTAB_FLOATS] verified softplus+quantize thresholds for dt_proj
+  unsigned* bar;    // [64] grid-barrier words of the fused decode kernel (zeroed at create)
 };
 
 extern "C" int qmb_abi_version(void) { return QMB_ABI_VERSION; }
@@ -232,7 +233,7 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
                o_wdt = take(w_dt_t.size()), o_dtb = take(E * 4), o_a = take((size_t)E * N * 4),
                o_acol = take((size_t)E * N), o_lut = take((size_t)128 * b->exp_ncols * 4), o_d = take(E * 4),
                o_wo = take(w_out_t.size()), o_luts = take(4 * 256 * 4), o_avals = take(a_vals.size() * 4),
-               o_qtab = take(QTAB_FLOATS * 4), o_scr = take(16),
+               o_qtab = take(QTAB_FLOATS * 4), o_scr = take(16), o_bar = take(256),
                o_etab = take(N == 16 ? (size_t)E * 128 * 16 * 4 : 0);
   cudaError_t e = cudaMalloc(&b->mem, off);
   if (e != cudaSuccess) {
@@ -255,6 +256,7 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
   b->luts = (float*)(base + o_luts);
   float* avals_dev = (float*)(base + o_avals);
   b->sp_qtab = (float*)(base + o_qtab);
+  b->bar = (unsigned*)(base + o_bar);
   uint32_t* scratch = (uint32_t*)(base + o_scr);
   struct Up {
     void* dst;
@@ -276,7 +278,8 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
       return cuda_fail(e, "qmb_block_create: upload");
     }
   }
-  e = build_exp_lut(b->luts + 256, avals_dev, b->exp_ncols, b->exp_lut, 0);
+  e = cudaMemset(b->bar, 0, 256);
+  if (e == cudaSuccess) e = build_exp_lut(b->luts + 256, avals_dev, b->exp_ncols, b->exp_lut, 0);
   if (e == cudaSuccess && b->exp_tab) e = build_exp_tab(b->luts + 256, b->a_deq, E, b->exp_tab, 0);
   if (e == cudaSuccess) e = build_softplus_qtab(f32(d->act[QMB_ACT_DT]), b->qmax, b->sp_qtab, scratch, 0);
   // verified conv silu+quantize fast path for this layer's scale (cached)
@@ -351,6 +354,18 @@ static int decode_scan_mode() {
 
 // Where the gate's silu(z) is evaluated: the in_proj epilogue (default) or the
 // scan (QMB_ZSILU_IN_GEMM=0, kept for A/B measurements).  Same f32 values either way.
+// QMB_DECODE_MID=1 runs the decode middle (conv, x_proj, dt_proj, scan) as one
+// kernel with two grid barriers.  Bit-exact (tests run it), but measured slower
+// in CUDA-graph replay than the PDL-chained separate kernels (B = 64: 1.73 vs
+// 1.53 ms per 16 layers; B = 1: 0.72 vs 0.64 ms), so it is opt-in.
+static bool decode_mid_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("QMB_DECODE_MID");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 static bool zsilu_in_gemm() {
   static const bool v = [] {
     const char* e = getenv("QMB_ZSILU_IN_GEMM");
@@ -421,6 +436,63 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
   // conv + SiLU + requant (qblock.py:199-201 -> fused_qconv :126-143)
   const float s_conv = f32(b->act[QMB_ACT_CONV_IN] * b->s_conv_w);
   PROF(1, st);
+  if (decode && b->exp_tab && zsilu_in_gemm() && decode_mid_enabled() &&
+      (long long)decode_mid_grid(E) * B * b->Nx <= SPLITK_SCRATCH_INTS && decode_mid_ok(B, E, N, b->Kc, b->Nx, R, b->Rp)) {
+    // conv step, x_proj, dt_proj + softplus, scan step and gate in one kernel
+    DecodeMidParams dp{};
+    dp.xq = xq;
+    dp.z = z;
+    dp.conv_state = conv_state;
+    dp.conv_w = b->conv_w;
+    dp.conv_b = b->conv_b;
+    dp.Kc = b->Kc;
+    dp.s_conv = s_conv;
+    dp.s_xo = f32(b->act[QMB_ACT_X]);
+    dp.inv_xo = 1.0f / dp.s_xo;
+    dp.thr_xo = silu_quant_thr(dp.s_xo, b->qmax, st);
+    dp.w_x = b->w_x_t;
+    dp.ld_wx = b->Ep;
+    dp.Nx = b->Nx;
+    EpiParams& ep = dp.epx;
+    ep.nseg = 3;
+    ep.qmax = b->qmax;
+    ep.err = err;
+    const double s_x = b->act[QMB_ACT_X];
+    ep.seg[0] = EpiSeg{0, N, EPI_QUANT, f32(s_x * b->s_w_b * 1.0), f32(b->act[QMB_ACT_B]), bq, N, nullptr};
+    ep.seg[1] = EpiSeg{N, 2 * N, EPI_QUANT, f32(s_x * b->s_w_c * 1.0), f32(b->act[QMB_ACT_C]), cq, N, nullptr};
+    ep.seg[2] = EpiSeg{2 * N, 2 * N + R, EPI_QUANT, f32(s_x * b->s_w_dtr * 1.0), f32(b->act[QMB_ACT_DT_R]), dtr,
+                       b->Rp, nullptr};
+    for (int k = 0; k < 3; ++k) ep.seg[k].out_inv = 1.0f / ep.seg[k].out_div;  // RN f32 reciprocal
+    dp.xpart = acc32;
+    dp.bq = bq;
+    dp.cq = cq;
+    dp.dtr = dtr;
+    dp.ld_dtr = b->Rp;
+    dp.w_dt = b->w_dt_t;
+    dp.ld_wdt = b->Rp;
+    dp.R = R;
+    dp.dt_scale = f32(b->act[QMB_ACT_DT_R] * b->s_w_dt * 1.0);
+    dp.dt_bias = b->dt_bias;
+    dp.qtab = b->sp_qtab;
+    dp.dt_div = f32(b->act[QMB_ACT_DT]);
+    dp.dt_inv = 1.0f / dp.dt_div;
+    dp.lut_x = b->luts;
+    dp.lut_dt = b->luts + 256;
+    dp.lut_b = b->luts + 512;
+    dp.lut_c = b->luts + 768;
+    dp.exp_tab = b->exp_tab;
+    dp.d = b->d_deq;
+    dp.h = ssm_state;
+    dp.bar = b->bar;
+    dp.B = B;
+    dp.E = E;
+    dp.qmax = b->qmax;
+    dp.err = err;
+    QMB_CUDA(decode_mid(dp, st), "decode middle");
+    PROF(2, st);
+    PROF(3, st);
+    PROF(4, st);
+  } else {
   if (decode) {
     QMB_CUDA(conv_step(xq, E, conv_state, b->conv_w, b->conv_b, scanx, b->Ep, B, E, b->Kc, s_conv,
                        f32(b->act[QMB_ACT_X]), b->qmax, err, st),
@@ -513,6 +585,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     const int use_lut = scan_exp != 0 ? 0 : (decode ? decode_scan_mode() : 1);
     QMB_CUDA(selective_scan(sp, use_lut, st), "scan");
   }
+  }  // (unfused stages)
   // output quantization (qblock.py:211-214)
   PROF(5, st);
   if (b->had) {
@@ -644,7 +717,7 @@ extern "C" int qmb_quantize_f64(const double* x, long long n, double scale, int 
   if (bit_width < 2 || bit_width > 8) return fail(QMB_E_UNSUPP, "bit width must be in [2, 8]");
   if (n <= 0) return 0;
   long long blocks = (n + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > num_sms() * 16) blocks = num_sms() * 16;
   quantize_f64_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, n, scale, qmax_of(bit_width), out, err);
   QMB_CUDA(cudaGetLastError(), "quantize_f64");
   return 0;
@@ -743,17 +816,21 @@ __global__ void scan_tables_kernel(const int8_t* a_q, double s_a, const int8_t* 
   if (k < D) d[k] = __double2float_rn(__dmul_rn((double)d_q[k], s_d));
 }
 
+extern "C" size_t qmb_selective_scan_workspace_bytes(int D, int N) {
+  if (D <= 0 || N <= 0) return 0;
+  return (1024 + (size_t)D * N + (size_t)D) * sizeof(float);
+}
+
 extern "C" int qmb_selective_scan(const int8_t* a_q, double s_a, const int8_t* b_q, double s_b, const int8_t* c_q,
                                   double s_c, const int8_t* d_q, double s_d, const int8_t* dt_q, double s_dt,
                                   const int8_t* x_q, double s_x, int B, int T, int D, int N, float* h, int h_in,
-                                  float* y, uint32_t* err, qmb_stream_t stream) {
+                                  float* y, void* ws, size_t ws_bytes, uint32_t* err, qmb_stream_t stream) {
   if (B < 0 || T < 0 || D <= 0 || N <= 0) return fail(QMB_E_ARG, "scan argument shapes are inconsistent");
   if (N > 64) return fail(QMB_E_UNSUPP, "d_state > 64 is not supported");
   cudaStream_t st = (cudaStream_t)stream;
-  static thread_local std::map<std::pair<int, int>, float*> scratch;  // persistent per (D, N)
-  float*& buf = scratch[{D, N}];
-  const size_t nfl = 1024 + (size_t)D * N + D;
-  if (!buf) QMB_CUDA(cudaMalloc(&buf, nfl * 4), "scan scratch");
+  const size_t need = qmb_selective_scan_workspace_bytes(D, N);
+  if (!ws || ws_bytes < need) return fail(QMB_E_WS, "workspace too small: need %zu bytes", need);
+  float* buf = static_cast<float*>(ws);
   float* luts = buf;
   float* a = buf + 1024;
   float* d = a + (size_t)D * N;

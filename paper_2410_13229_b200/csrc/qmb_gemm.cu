@@ -770,6 +770,168 @@ __global__ void __launch_bounds__(256) gemm_i8_simt_kernel(const int8_t* __restr
   flag_error(ep.err, err);
 }
 
+// ============================================================ decode GEMV (M <= 8)
+// Decode-size products stream every weight byte once and do ~M int8 MACs per byte:
+// HBM-bound, so this path is built for bytes in flight rather than tensor-core
+// throughput.  CTA = GV_WC x WK warps; warp (wc, wk) owns 4 output columns
+// n0 + 4 wc .. + 3 and the K slice wk (lanes take 16 consecutive bytes each, 512 B
+// of K per warp-iteration).  The weight rows are K-major [N][ldb], so a warp's
+// loads are four fully-used 512-byte segments; GV_LA slices stay in flight per
+// warp (a register ring, each slot refilled as it is consumed), and the first
+// slice is issued before griddepcontrol.wait (weights never depend on the
+// previous kernel of a decode chain).  The M <= MB activation rows are staged in
+// shared memory once per CTA.  Per-warp int32 sums: xor-shuffle tree, then the
+// WK K-slices through shared memory -- exact in any order.  The epilogue is the
+// same per-element code as every other path (epi_store_one).
+constexpr int GV_WC = 4;  // column warps per CTA (16 columns)
+
+template <int MB, int WK>
+__global__ void __launch_bounds__(32 * GV_WC * WK) gemv_i8_kernel(const int8_t* __restrict__ A, long long lda,
+                                                                 const int8_t* __restrict__ Bt, long long ldb, int M,
+                                                                 int N, int Kp, EpiParams ep) {
+  extern __shared__ __align__(16) uint8_t gv_smem[];
+  int8_t* sA = reinterpret_cast<int8_t*>(gv_smem);                         // [MB][Kp]
+  int* sRed = reinterpret_cast<int*>(gv_smem + ((MB * Kp + 15) & ~15));   // [WK][4 GV_WC][MB]
+  __shared__ float sQt[QTAB_FLOATS];
+  const float* qt = stage_qtab(ep, sQt);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wc = warp % GV_WC, wk = warp / GV_WC;
+  const int n0 = (blockIdx.x * GV_WC + wc) * 4;
+  const int nslices = Kp / 512 + ((Kp & 511) ? 1 : 0);
+  const int per = (nslices + WK - 1) / WK;
+  const int s0 = wk * per, s1 = min(nslices, s0 + per);
+  const int8_t* brow[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) brow[j] = Bt + (long long)min(n0 + j, N - 1) * ldb;
+  auto ldw = [&](int sl, int4 (&w)[4]) {
+    const int k = sl * 512 + lane * 16;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      w[j] = (sl < s1 && k < Kp) ? __ldg(reinterpret_cast<const int4*>(brow[j] + k)) : make_int4(0, 0, 0, 0);
+  };
+  int4 wcur[4];
+  ldw(s0, wcur);  // before the dependency wait
+  pdl_wait();
+  pdl_trigger();
+  for (int k = threadIdx.x * 16; k < MB * Kp; k += blockDim.x * 16) {
+    const int m = k / Kp, kk = k - m * Kp;
+    *reinterpret_cast<int4*>(sA + k) =
+        m < M ? *reinterpret_cast<const int4*>(A + (long long)m * lda + kk) : make_int4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  int acc[4][MB];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int m = 0; m < MB; ++m) acc[j][m] = 0;
+  // GV_LA slices (512 B x 4 columns each) in flight per warp: a register ring,
+  // refilled as each slice is used (fewer for many rows: their accumulators)
+  constexpr int GV_LA = 2;  // (deeper rings measured slower: fewer CTAs resident per SM)
+  int4 wr[GV_LA - 1][4];
+#pragma unroll
+  for (int u = 0; u < GV_LA - 1; ++u) ldw(s0 + 1 + u, wr[u]);
+  for (int sl = s0; sl < s1; sl += GV_LA) {
+#pragma unroll
+    for (int u = 0; u < GV_LA; ++u) {
+      int4 wc[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) wc[j] = u == 0 ? wcur[j] : wr[u - 1][j];
+      // refill this ring slot with the slice GV_LA ahead
+      if (u == 0) ldw(sl + GV_LA, wcur); else ldw(sl + u + GV_LA, wr[u - 1]);
+      const int k = (sl + u) * 512 + lane * 16;
+      if (sl + u < s1 && k < Kp) {
+#pragma unroll
+        for (int m = 0; m < MB; ++m) {
+          const int4 a = *reinterpret_cast<const int4*>(sA + m * Kp + k);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[j][m] = __dp4a(a.x, wc[j].x, acc[j][m]);
+            acc[j][m] = __dp4a(a.y, wc[j].y, acc[j][m]);
+            acc[j][m] = __dp4a(a.z, wc[j].z, acc[j][m]);
+            acc[j][m] = __dp4a(a.w, wc[j].w, acc[j][m]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int m = 0; m < MB; ++m)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[j][m] += __shfl_xor_sync(0xffffffffu, acc[j][m], o);
+  if (WK > 1) {
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int m = 0; m < MB; ++m) sRed[(wk * 4 * GV_WC + 4 * wc + j) * MB + m] = acc[j][m];
+    }
+    __syncthreads();
+  }
+  // output (column j of this warp, row m) -> lane 8 j + m ... (MB <= 8)
+  if (wk == 0) {
+    const int j = lane >> 3, m = lane & 7;
+    if (m < MB && m < M && n0 + j < N) {
+      int v = 0;
+      if (WK > 1) {
+#pragma unroll
+        for (int w = 0; w < WK; ++w) v += sRed[(w * 4 * GV_WC + 4 * wc + j) * MB + m];
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int mm = 0; mm < MB; ++mm)
+            if (jj == j && mm == m) v = acc[jj][mm];
+      }
+      uint32_t err = 0;
+      int oc;
+      const EpiSeg sg = pick_seg(ep, epi_locate(ep, n0 + j, &oc));
+      epi_store_one(ep, sg, m, oc, v, err, qt);
+      flag_error(ep.err, err);
+    }
+  }
+}
+
+template <int MB>
+static cudaError_t launch_gemv_mb(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N,
+                                  int Kp, const EpiParams& ep, cudaStream_t st) {
+  const int ctas = (N + 4 * GV_WC - 1) / (4 * GV_WC);
+  const int nslices = (Kp + 511) / 512;
+  // K split across warps when there are too few column CTAs to keep every SM streaming
+  const int wk = (ctas >= 2 * num_sms() || nslices < 2) ? 1 : (ctas * 2 >= num_sms() || nslices < 4 ? 2 : 4);
+  const size_t smem = (size_t)((MB * Kp + 15) & ~15) + (size_t)4 * 4 * GV_WC * MB * 4;
+  if (wk == 1) {
+    cudaError_t e = ensure_smem_attr((const void*)gemv_i8_kernel<MB, 1>, smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(M <= 128, gemv_i8_kernel<MB, 1>, dim3((unsigned)ctas), dim3(32 * GV_WC), smem, st, A, lda, Bt,
+                      ldb, M, N, Kp, ep);
+  }
+  if (wk == 2) {
+    cudaError_t e = ensure_smem_attr((const void*)gemv_i8_kernel<MB, 2>, smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(M <= 128, gemv_i8_kernel<MB, 2>, dim3((unsigned)ctas), dim3(64 * GV_WC), smem, st, A, lda, Bt,
+                      ldb, M, N, Kp, ep);
+  }
+  cudaError_t e = ensure_smem_attr((const void*)gemv_i8_kernel<MB, 4>, smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(M <= 128, gemv_i8_kernel<MB, 4>, dim3((unsigned)ctas), dim3(128 * GV_WC), smem, st, A, lda, Bt,
+                    ldb, M, N, Kp, ep);
+}
+
+static bool gemv_ok(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int Kp) {
+  return M >= 1 && M <= 8 && Kp % 16 == 0 && lda % 16 == 0 && ldb % 16 == 0 && (uintptr_t)A % 16 == 0 &&
+         (uintptr_t)Bt % 16 == 0 && (size_t)8 * Kp <= 160 * 1024;
+}
+
+static cudaError_t launch_gemv(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
+                               const EpiParams& ep, cudaStream_t st) {
+  if (M <= 1) return launch_gemv_mb<1>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+  if (M <= 2) return launch_gemv_mb<2>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+  if (M <= 4) return launch_gemv_mb<4>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+  return launch_gemv_mb<8>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+}
+
 // ============================================================ int8 tensor peak probe
 // One CTA per SM issues back-to-back M=128 x N=256 x K=32 kind::i8 MMAs on
 // resident smem operands (no TMA, no epilogue): the measured int8 dense peak
@@ -858,14 +1020,16 @@ bool make_tmap_3d(CUtensorMap* tm, int elem, const void* base, const long long d
 }
 
 int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+    cache[dev] = n > 0 ? n : 148;
   }
-  return n;
+  return cache[dev];
 }
 
 // Store map for one epilogue segment: f32 as 32x16 boxes (SWIZZLE_64B), int8 as
@@ -904,12 +1068,9 @@ static cudaError_t launch_tc(const int8_t* A, long long lda, const int8_t* Bt, l
   } else {
     ep.tma_seg = ep.tma_seg2 = -1;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc_kernel<BN, EPIW, TMAOUT, CG>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+  {
+    cudaError_t e = ensure_smem_attr((const void*)gemm_i8_tc_kernel<BN, EPIW, TMAOUT, CG>, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const int tiles = ((M + TC_BM * CG - 1) / (TC_BM * CG)) * ((N + BN - 1) / BN) * (ep.splitk > 1 ? ep.splitk : 1);
   const int slots = num_sms() / CG;
@@ -1115,6 +1276,9 @@ cudaError_t gemm_bench(int M, int N, int K, int mode, int iters, float* ms_out) 
 // Epilogue of a split-K GEMM: the exact int32 sums in acc32 [M, N] through the
 // same per-element float steps as the fused epilogue.
 __global__ void epi_apply_kernel(const int32_t* __restrict__ acc, int splitk, int M, int N, EpiParams ep) {
+  __shared__ float sQt[QTAB_FLOATS];
+  const float* qt = stage_qtab(ep, sQt);
+  __syncthreads();
   pdl_wait();
   pdl_trigger();
   uint32_t err = 0;
@@ -1134,7 +1298,7 @@ __global__ void epi_apply_kernel(const int32_t* __restrict__ acc, int splitk, in
     const int s = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
     int oc;
     const EpiSeg sg = pick_seg(ep, epi_locate(ep, n, &oc));
-    epi_store_one(ep, sg, m, oc, s, err);
+    epi_store_one(ep, sg, m, oc, s, err, qt);
   }
   flag_error(ep.err, err);
 }
@@ -1166,9 +1330,25 @@ static cudaError_t launch_tc_choose(const int8_t* A, long long lda, const int8_t
   ep.splitk = 1;
   const long long total = (long long)M * N;
   long long blocks = (total + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
   return launch_pdl(true, epi_apply_kernel, dim3((unsigned)blocks), dim3(256), 0, st, (const int32_t*)acc32, splitk, M,
                     N, ep);
+}
+
+static bool gemm_spin() {
+  static const bool v = [] {
+    const char* e = getenv("QMB_GEMM_SPIN");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+static bool gemv_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("QMB_GEMV");
+    return !(e && !strcmp(e, "0"));
+  }();
+  return v;
 }
 
 cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
@@ -1177,7 +1357,7 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
   EpiParams ep = ep_in;
   ep.splitk = 1;
   ep.acc32 = nullptr;
-  ep.spin = 0;  // (spinning waits measured no faster for decode-size GEMMs)
+  ep.spin = (M <= TC_BM && gemm_spin()) ? 1 : 0;  // QMB_GEMM_SPIN=1: spinning pipeline waits for decode GEMMs
   ep.small_acc = (long long)Kp * 128 * 128 < (1LL << 22) ? 1 : 0;
   ep.qtab_bias = QTAB_BIAS;
   ep.one2 = kOne2;
@@ -1186,6 +1366,12 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
   const bool tc_ok = (lda % 16 == 0) && (ldb % 16 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)Bt % 16 == 0) &&
                      Kp > 0;
   int path = force_path;
+  // decode-size M: the streaming GEMV (path 3); QMB_GEMV=0 keeps the tensor-core split-K path
+  if (path == 0 && gemv_enabled() && gemv_ok(A, lda, Bt, ldb, M, Kp)) path = 3;
+  if (path == 3) {
+    if (!gemv_ok(A, lda, Bt, ldb, M, Kp)) return cudaErrorInvalidValue;
+    return launch_gemv(A, lda, Bt, ldb, M, N, Kp, ep, st);
+  }
   if (path == 0) path = (tc_ok && (M > 16 || acc32)) ? 1 : 2;
   if (path == 1 && !tc_ok) return cudaErrorInvalidValue;
   if (path == 1) {

@@ -172,10 +172,24 @@ __device__ __forceinline__ int epi_locate(const EpiParams& ep, int n, int* ocol)
   return s;
 }
 
-// One output element, scalar path (shared by the SIMT kernel and ragged tiles);
-// oc = output column within segment sg.
+// Stage the (single) EPI_SOFTPLUS_Q segment's threshold table into shared memory
+// (QTAB_FLOATS floats at dst); returns dst, or null when no segment needs it.
+// Call from every thread of the CTA, then __syncthreads().
+__device__ __forceinline__ const float* stage_qtab(const EpiParams& ep, float* dst) {
+  const float* src = nullptr;
+  for (int s = 0; s < ep.nseg; ++s)
+    if (ep.seg[s].kind == EPI_SOFTPLUS_Q) src = ep.seg[s].qtab;
+  if (!src) return nullptr;
+  for (int k = threadIdx.x; k < QTAB_FLOATS; k += blockDim.x) dst[k] = src[k];
+  return dst;
+}
+
+// One output element, scalar path (shared by the SIMT / GEMV / split-K fix-up
+// kernels); oc = output column within segment sg.  sqtab: the softplus threshold
+// table staged in SHARED memory (the table function reads it with ld.shared), or
+// null for the exact evaluation.
 __device__ __forceinline__ void epi_store_one(const EpiParams& ep, const EpiSeg& sg, long long m, int oc, int acc,
-                                              uint32_t& err) {
+                                              uint32_t& err, const float* sqtab = nullptr) {
   float v = __fmul_rn(__int2float_rn(acc), sg.acc_scale);
   if (sg.bias) v = __fadd_rn(v, sg.bias[oc]);
   long long off = m * sg.ld + oc;
@@ -183,7 +197,7 @@ __device__ __forceinline__ void epi_store_one(const EpiParams& ep, const EpiSeg&
     float* o = static_cast<float*>(sg.out) + off;
     *o = sg.kind == EPI_F32_SILU ? silu_f32_fast(v) : (sg.kind == EPI_F32_ADDTO ? __fadd_rn(v, *o) : v);
   } else if (sg.kind == EPI_SOFTPLUS_Q) {
-    static_cast<int8_t*>(sg.out)[off] = (int8_t)softplus_quant(v, sg.qtab, sg.out_div, sg.out_inv, ep.qmax, err);
+    static_cast<int8_t*>(sg.out)[off] = (int8_t)softplus_quant(v, sqtab, sg.out_div, sg.out_inv, ep.qmax, err);
   } else {
     static_cast<int8_t*>(sg.out)[off] = (int8_t)quant_fast(v, sg.out_div, sg.out_inv, ep.qmax, err);
   }

@@ -289,10 +289,12 @@ def quantized_selective_scan(a_q, b_q, c_q, d_q, dt_q, x_q, h0=None, return_stat
         else:
             h = torch.zeros((B, D, N), dtype=torch.float32, device=x.device)
     err = _device.err_flag()
+    nws = _lib.load().qmb_selective_scan_workspace_bytes(int(D), int(N))
+    ws = torch.empty(max(int(nws), 1), dtype=torch.uint8, device=x.device)
     _lib.call("qmb_selective_scan", a.data_ptr(), float(a_q.scale), bq.data_ptr(), float(b_q.scale), cq.data_ptr(),
               float(c_q.scale), dd.data_ptr(), float(d_q.scale), dt.data_ptr(), float(dt_q.scale), x.data_ptr(),
               float(x_q.scale), int(B), int(T), int(D), int(N), _device.ptr(h), int(h0 is not None),
-              y.data_ptr(), err.ptr, _device.stream_ptr())
+              y.data_ptr(), ws.data_ptr(), ws.numel(), err.ptr, _device.stream_ptr())
     y = y.reshape(x.shape)
     yv = _finish(y, as_numpy)
     if not return_state:

@@ -155,8 +155,9 @@ def test_block_small_batch_bit_exact(cuda, oracle, name, B, T):
         assert np.array_equal(hs[b].view(np.uint32), st["h"].view(np.uint32)), b
 
 
-@pytest.mark.parametrize("name", ["tiny_full", "m12_full", "p2_inper", "s2p8b"])
-def test_block_decode_equals_prefill(cuda, name):
+@pytest.mark.parametrize("name,B", [("tiny_full", 2), ("m12_full", 2), ("p2_inper", 2), ("s2p8b", 2), ("s2p8b", 37),
+                                    ("s130m", 5), ("m20_full", 64)])
+def test_block_decode_equals_prefill(cuda, name, B):
     """Prefill k tokens (exporting state), then decode the rest one by one: every
     decoded row and the final state equal the one-shot prefill bit-for-bit."""
     from paper_2410_13229_b200 import _device
@@ -167,7 +168,6 @@ def test_block_decode_equals_prefill(cuda, name):
     dev = device_block(qb)
     u = torch.from_numpy(z["u_q"]).cuda()
     T, D = u.shape
-    B = 2
     ub = u[None].repeat(B, 1, 1).contiguous()
     k = T // 2
     conv, h = dev.new_state(B)
@@ -217,3 +217,19 @@ def test_block_accumulate_is_the_residual_add(cuda, name):
     dev.decode(u[:B].contiguous(), conv2, h2, acc, u_scale=meta["u_scale"], accumulate=True)
     _device.err_flag().raise_if_set()
     assert np.array_equal(acc.cpu().numpy().view(np.uint32), (row.cpu().numpy() + res0[:B]).view(np.uint32))
+
+
+def test_fused_decode_middle_bit_exact(cuda):
+    """QMB_DECODE_MID=1 (opt-in): conv step, x_proj, dt_proj + softplus and the scan
+    step in one kernel with two grid barriers -- the decode-equals-prefill checks
+    rerun in a fresh process with it enabled."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    here = Path(__file__).resolve().parent
+    env = dict(os.environ, QMB_DECODE_MID="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", str(here / "test_gpu_block.py"),
+                        "-k", "decode_equals_prefill"], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
