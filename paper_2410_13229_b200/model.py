@@ -84,12 +84,17 @@ class DeviceModel:
         self.embedding = _f32_dev(model.embedding)
         self.final_norm = _f32_dev(model.final_norm)
         self.norms = [_f32_dev(l.norm_weight) for l in model.layers]
+        # the norm kernels range-check their input, not gain: a non-finite gain would make
+        # every forward's quantize raise in the reference (quant.py:149-150), so refuse it here
+        self.gains_finite = all(bool(torch.isfinite(g).all()) for g in self.norms + [self.final_norm])
         self.s_in = [float(l.block.act["in"].scale) for l in model.layers]
         self.blocks: list[DeviceBlock] = [device_block(l.block) for l in model.layers]
         self._lib = _lib.load()
 
     # ---------------------------------------------------------------- pieces
     def _rmsnorm(self, x_out, x_res, res_out, gain, s_out, u_q, y_out, M, err, stream):
+        if not self.gains_finite and M > 0:
+            raise ValueError("non-finite activation")
         _lib.check(self._lib.qmb_rmsnorm_residual_quant(
             x_out.data_ptr(), _device.ptr(x_res), _device.ptr(res_out), gain.data_ptr(), int(M), self.D,
             float(s_out), self.bits, _device.ptr(u_q), _device.ptr(y_out), err.ptr, stream), "rmsnorm")
@@ -238,10 +243,17 @@ class DeviceModel:
 
 
 def device_model(model) -> DeviceModel:
+    """The device mirror of a QuantizedModel, cached on the object; rebuilt when the
+    embedding / norm arrays are replaced (each block's handle revalidates itself)."""
     dm = model.__dict__.get("_qmb_device_model")
-    if dm is None:
+    fp = (id(model.embedding), id(model.final_norm), tuple(id(l.norm_weight) for l in model.layers),
+          tuple(id(l.block) for l in model.layers))
+    if dm is None or model.__dict__.get("_qmb_device_model_fp") != fp:
         dm = DeviceModel(model)
         model.__dict__["_qmb_device_model"] = dm
+        model.__dict__["_qmb_device_model_fp"] = fp
+    else:
+        dm.blocks = [device_block(l.block) for l in model.layers]
     return dm
 
 

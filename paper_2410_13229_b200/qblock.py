@@ -188,12 +188,25 @@ class DeviceBlock:
         return conv, h
 
 
+def _block_fingerprint(qb) -> tuple:
+    """Identity of what a device handle was built from: the weight arrays (object
+    ids and buffer addresses) and every weight / activation scale.  The reference's
+    QuantizedBlock is a mutable dataclass (qblock.py:75-95): re-calibrating it or
+    swapping a weight changes this, and the next call rebuilds the handle."""
+    w = tuple((k, id(v), id(getattr(v, "values", None)), float(v.scale)) for k, v in sorted(qb.weights.items()))
+    a = tuple((k, float(v.scale)) for k, v in sorted(qb.act.items()))
+    return w, a, _mode_value(qb.mode), id(qb.plan)
+
+
 def device_block(qb) -> DeviceBlock:
-    """The (cached) device handle of a QuantizedBlock (reference or mirror object)."""
+    """The device handle of a QuantizedBlock (reference or mirror object), cached
+    on the object and rebuilt when its weights or scales change."""
     dev = qb.__dict__.get("_qmb_device")
-    if dev is None:
+    fp = _block_fingerprint(qb)
+    if dev is None or qb.__dict__.get("_qmb_device_fp") != fp:
         dev = DeviceBlock(qb)
         qb.__dict__["_qmb_device"] = dev
+        qb.__dict__["_qmb_device_fp"] = fp
     return dev
 
 
@@ -311,6 +324,10 @@ def fused_rmsnorm_quant(x_out, x_res, gain, s_out: float, bit_width: int = 8):
     g = _device.to_device(np.asarray(gain, dtype=np.float32) if not is_device(gain) else gain, torch.float32)
     D = xo.shape[-1]
     M = xo.numel() // D
+    if M > 0 and not bool(torch.isfinite(g).all()):
+        # a non-finite gain makes that column of every normalized row non-finite:
+        # the reference's quantize raises (quant.py:149-150)
+        raise ValueError("non-finite activation")
     res = torch.empty_like(xo)
     u = torch.empty(xo.shape, dtype=torch.int8, device=xo.device)
     err = _device.err_flag()

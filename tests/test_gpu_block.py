@@ -233,3 +233,36 @@ def test_fused_decode_middle_bit_exact(cuda):
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", str(here / "test_gpu_block.py"),
                         "-k", "decode_equals_prefill"], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_handle_rebuilt_when_block_is_recalibrated(cuda, oracle):
+    """The device handle cached on a QuantizedBlock is rebuilt when its scales change
+    (the reference's QuantizedBlock is a mutable dataclass, qblock.py:75-95)."""
+    from paper_2410_13229_b200 import QTensor, block_forward_q
+    from paper_2410_13229_b200.qblock import ScaleEntry
+
+    z, meta = load_block("m20_full")
+    w = block_weights(z, meta)
+    qb = mirror_block(z, meta, w)
+    u = QTensor(z["u_q"], meta["u_scale"])
+    first = block_forward_q(u, qb)
+    assert np.array_equal(first.view(np.uint32), z["st_out"].view(np.uint32))
+    # re-calibrate one site in place, as run_calibration + quantize_block would
+    old = qb.act["y_had"]
+    qb.act["y_had"] = ScaleEntry(old.scale * 1.5, old.zero_point, old.scheme)
+    meta2 = dict(meta, act=dict(meta["act"], y_had=old.scale * 1.5))
+    ob2 = oracle_block(z, meta2, w)
+    ref2 = oracle.block_forward_q(z["u_q"], meta["u_scale"], ob2)
+    second = block_forward_q(u, qb)
+    assert np.array_equal(second.view(np.uint32), ref2.view(np.uint32))
+    assert not np.array_equal(second, first)
+
+
+def test_nonfinite_gain_raises(cuda):
+    from paper_2410_13229_b200 import fused_rmsnorm_quant
+
+    x = np.ones((3, 16), dtype=np.float32)
+    g = np.ones(16, dtype=np.float32)
+    g[5] = np.nan
+    with pytest.raises(ValueError, match="non-finite activation"):
+        fused_rmsnorm_quant(x, np.zeros_like(x), g, 0.05)
