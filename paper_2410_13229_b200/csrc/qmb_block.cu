@@ -366,6 +366,15 @@ static bool decode_mid_enabled() {
   return v;
 }
 
+// QMB_DECODE_SCAN_FUSED=0 keeps dt_proj and the split-K fix-up as separate decode kernels.
+static bool decode_scan_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("QMB_DECODE_SCAN_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 static bool zsilu_in_gemm() {
   static const bool v = [] {
     const char* e = getenv("QMB_ZSILU_IN_GEMM");
@@ -518,6 +527,9 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
   }
   // x_proj: b, c, dt_r (qblock.py:202-204)
   PROF(2, st);
+  bool fused_dscan = false;
+  int xsplit = 0;
+  EpiParams xepi{};
   {
     EpiParams ep{};
     ep.nseg = 3;
@@ -528,11 +540,56 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     ep.seg[1] = EpiSeg{N, 2 * N, EPI_QUANT, f32(s_x * b->s_w_c * 1.0), f32(b->act[QMB_ACT_C]), cq, N, nullptr};
     ep.seg[2] = EpiSeg{2 * N, 2 * N + R, EPI_QUANT, f32(s_x * b->s_w_dtr * 1.0), f32(b->act[QMB_ACT_DT_R]), dtr,
                        b->Rp, nullptr};
-    QMB_CUDA(gemm_i8(scanx, b->Ep, b->w_x_t, b->Ep, (int)M, b->Nx, E, ep, st, 0, acc32), "x_proj gemm");
+    // (B <= 8: x_proj runs as the GEMV with its epilogue; at larger B the per-row finish
+    // of x_proj's split-K partials inside the scan kernel measured slower than the
+    // separate fix-up + dt_proj kernels: B = 64, 16 layers 1.73 vs 1.54 ms)
+    fused_dscan = decode && B <= 8 && b->exp_tab && zsilu_in_gemm() && decode_scan_enabled() &&
+                  decode_scan_ok(B, E, N, b->Nx, R, b->Rp);
+    // fused decode scan: x_proj may leave its split-K partials for the scan kernel to finish
+    QMB_CUDA(gemm_i8(scanx, b->Ep, b->w_x_t, b->Ep, (int)M, b->Nx, E, ep, st, 0, acc32,
+                     fused_dscan ? &xsplit : nullptr),
+             "x_proj gemm");
+    xepi = ep;
   }
   // dt_proj + bias + softplus + quantize (qblock.py:205-206)
   PROF(3, st);
-  {
+  if (fused_dscan) {
+    // dt_proj, softplus, the scan step and the gate in one kernel (+ the x_proj finish)
+    DecodeScanParams dp{};
+    dp.x = scanx;
+    dp.ldx = b->Ep;
+    dp.z = z;
+    dp.splitk = xsplit;
+    dp.xpart = acc32;
+    dp.Nx = b->Nx;
+    dp.epx = xepi;
+    for (int k = 0; k < 3; ++k) dp.epx.seg[k].out_inv = 1.0f / dp.epx.seg[k].out_div;  // RN f32 reciprocal
+    dp.bq = bq;
+    dp.cq = cq;
+    dp.dtr = dtr;
+    dp.ld_dtr = b->Rp;
+    dp.w_dt = b->w_dt_t;
+    dp.ld_wdt = b->Rp;
+    dp.R = R;
+    dp.dt_scale = f32(b->act[QMB_ACT_DT_R] * b->s_w_dt * 1.0);
+    dp.dt_bias = b->dt_bias;
+    dp.qtab = b->sp_qtab;
+    dp.dt_div = f32(b->act[QMB_ACT_DT]);
+    dp.dt_inv = 1.0f / dp.dt_div;
+    dp.lut_x = b->luts;
+    dp.lut_dt = b->luts + 256;
+    dp.lut_b = b->luts + 512;
+    dp.lut_c = b->luts + 768;
+    dp.exp_tab = b->exp_tab;
+    dp.d = b->d_deq;
+    dp.h = ssm_state;
+    dp.B = B;
+    dp.E = E;
+    dp.qmax = b->qmax;
+    dp.err = err;
+    QMB_CUDA(decode_scan(dp, st), "decode scan");
+    PROF(4, st);
+  } else {
     EpiParams ep{};
     ep.nseg = 1;
     ep.qmax = b->qmax;
@@ -540,10 +597,8 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     ep.seg[0] = EpiSeg{0, E, EPI_SOFTPLUS_Q, f32(b->act[QMB_ACT_DT_R] * b->s_w_dt * 1.0), f32(b->act[QMB_ACT_DT]),
                        delta, E, b->dt_bias, b->sp_qtab};
     QMB_CUDA(gemm_i8(dtr, b->Rp, b->w_dt_t, b->Rp, (int)M, E, R, ep, st, 0, acc32), "dt_proj gemm");
-  }
-  // scan + D skip + gate (qblock.py:207-210), gated y written over z
-  PROF(4, st);
-  {
+    // scan + D skip + gate (qblock.py:207-210), gated y written over z
+    PROF(4, st);
     ScanParams sp{};
     sp.x = scanx;
     sp.ldx = b->Ep;
@@ -584,7 +639,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     // (decode, one step per sequence), 0: direct FP64 glibc-expf restatement
     const int use_lut = scan_exp != 0 ? 0 : (decode ? decode_scan_mode() : 1);
     QMB_CUDA(selective_scan(sp, use_lut, st), "scan");
-  }
+  }  // (unfused dt_proj + scan)
   }  // (unfused stages)
   // output quantization (qblock.py:211-214)
   PROF(5, st);

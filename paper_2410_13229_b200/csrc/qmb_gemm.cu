@@ -1307,7 +1307,7 @@ __global__ void epi_apply_kernel(const int32_t* __restrict__ acc, int splitk, in
 
 template <int BN>
 static cudaError_t launch_tc_choose(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N,
-                                    int Kp, EpiParams ep, cudaStream_t st, int32_t* acc32) {
+                                    int Kp, EpiParams ep, cudaStream_t st, int32_t* acc32, int* defer = nullptr) {
   const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
   const int num_k = (Kp + TC_BK - 1) / TC_BK;
   int splitk = 1;
@@ -1327,6 +1327,10 @@ static cudaError_t launch_tc_choose(const int8_t* A, long long lda, const int8_t
   sp.tma_seg = sp.tma_seg2 = -1;
   cudaError_t e = launch_tc<BN, 8, false>(A, lda, Bt, ldb, M, N, Kp, sp, st);
   if (e != cudaSuccess) return e;
+  if (defer) {  // the caller's next kernel sums the splitk partials and runs the epilogue
+    *defer = splitk;
+    return cudaSuccess;
+  }
   ep.splitk = 1;
   const long long total = (long long)M * N;
   long long blocks = (total + 255) / 256;
@@ -1352,7 +1356,8 @@ static bool gemv_enabled() {
 }
 
 cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
-                    const EpiParams& ep_in, cudaStream_t st, int force_path, int32_t* acc32) {
+                    const EpiParams& ep_in, cudaStream_t st, int force_path, int32_t* acc32, int* defer) {
+  if (defer) *defer = 0;
   if (M <= 0 || N <= 0) return cudaSuccess;
   EpiParams ep = ep_in;
   ep.splitk = 1;
@@ -1378,21 +1383,21 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
     if (M > TC_BM) acc32 = nullptr;  // split-K only for skinny (decode-like) M
     // skinny M: one wave of 96-column tiles beats two waves of 64-column ones
     if (M <= TC_BM && N > 192 && (N + 63) / 64 > num_sms() && (N + 95) / 96 <= num_sms())
-      return launch_tc_choose<96>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
+      return launch_tc_choose<96>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
     // Column tile: the largest BN that still gives >= 1 wave, else the smallest.
-    if (N <= 32) return launch_tc_choose<32>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
-    if (N <= 64) return launch_tc_choose<64>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
-    if (N <= 128) return launch_tc_choose<128>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
-    if (N <= 192) return launch_tc_choose<192>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
+    if (N <= 32) return launch_tc_choose<32>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
+    if (N <= 64) return launch_tc_choose<64>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
+    if (N <= 128) return launch_tc_choose<128>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
+    if (N <= 192) return launch_tc_choose<192>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
     const long long m_tiles = (M + TC_BM - 1) / TC_BM;
     // CTA pairs (256 x 256 tiles) once there are enough pair tiles for every SM pair
     if (gemm_pair_enabled() && ((M + 255) / 256) * ((N + 255) / 256) >= num_sms() / 2)
       return launch_tc_bn<256, 2>(A, lda, Bt, ldb, M, N, Kp, ep, st);
     if (m_tiles * ((N + 255) / 256) >= num_sms())
-      return launch_tc_choose<256>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
+      return launch_tc_choose<256>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
     if (m_tiles * ((N + 127) / 128) >= num_sms())
-      return launch_tc_choose<128>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
-    return launch_tc_choose<64>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32);
+      return launch_tc_choose<128>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
+    return launch_tc_choose<64>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
   }
   const int vec = ((lda % 16) == 0 && (ldb % 16) == 0 && ((uintptr_t)A % 16) == 0 && ((uintptr_t)Bt % 16) == 0);
   constexpr int MB = 8;

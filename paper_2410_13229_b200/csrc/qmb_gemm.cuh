@@ -215,8 +215,11 @@ namespace qmb {
 // SMs streaming weights.
 constexpr long long SPLITK_SCRATCH_INTS = 148LL * 128 * 256;
 cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
-                    const EpiParams& ep, cudaStream_t st, int force_path /*0 auto, 1 tc, 2 simt*/,
-                    int32_t* acc32_scratch = nullptr);
+                    const EpiParams& ep, cudaStream_t st, int force_path /*0 auto, 1 tc, 2 simt, 3 gemv*/,
+                    int32_t* acc32_scratch = nullptr, int* defer_splitk = nullptr);
+// defer_splitk (nullable): when the launch splits K (skinny M with acc32_scratch), skip
+// the fix-up kernel and return the split count here (the int32 partials are left in
+// acc32_scratch as [split][M][N] for the caller's next kernel); 0 = the epilogue ran.
 int num_sms();
 // Tiled TMA map of a rank-3 tensor: dims innermost first, byte strides of dims 1, 2;
 // elem 1 = uint8, 4 = float32; swizzle 0 / 64 / 128 (bytes).
