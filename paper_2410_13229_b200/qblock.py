@@ -125,6 +125,8 @@ class DeviceBlock:
                      "w_out_h"):
             if name not in qb.weights:
                 continue
+            if name == "w_out" and "w_out_h" in qb.weights and qb.mode.hadamard_output:
+                continue  # the handle runs the fused w_out_h (container loads never page w_out in)
             w = qb.weights[name]
             if w.zero_point:
                 raise ValueError("qlinear requires symmetric operands")
