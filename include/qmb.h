@@ -147,6 +147,36 @@ int qmb_block_decode(const qmb_block* blk, const int8_t* u_q, double u_scale, in
 /* Prefill with per-stage device timing (CUDA events on `stream`; synchronizes).
  * stage_ms: in_proj, conv, x_proj, dt_proj, scan, output quant, out_proj. */
 #define QMB_NUM_STAGES 7
+/* Tensor-parallel E-sharding: a handle created from a
+ * contiguous channel slice [e0, e0 + d_inner) of a block (w_in's x and z columns,
+ * conv, a, d, dt_bias and w_dt's columns of those channels; w_b / w_c / w_dt_rank
+ * and w_out(_h) rows of those channels as K-slices; every scale unchanged) runs
+ * one layer in four stages around three collectives:
+ *   1  in_proj, conv, x_proj partial    -> xacc  [M, 2N + R] int32   (all-reduce SUM)
+ *   2  x_proj requant, dt_proj, scan    -> y_local [M, d_inner] f32  (all-gather over channels)
+ *   3  Hadamard (FULL plan) of y_full, out_proj partial of the local K-slice
+ *                                       -> oacc  [M, D] int32        (all-reduce SUM)
+ *   4  out_proj epilogue (+= out if accumulate)
+ * The int32 sums are exact in any order: the result is bit-identical to the
+ * unsharded qmb_block_prefill / qmb_block_decode.  The same workspace must be
+ * passed to every stage of a step; conv_state / ssm_state are the local
+ * channels' (decode: in-out; prefill: outputs, nullable). */
+typedef struct {
+  int stage;                 /* 1..4 */
+  int32_t* xacc;             /* [M, 2N + R] */
+  float* y_local;            /* [M, d_inner] */
+  const float* y_full;       /* [M, e_full] */
+  int8_t* yq_full;           /* [M, e_full] scratch */
+  long long e_full;          /* full d_inner (multiple of 16) */
+  int e0;                    /* first channel of this handle (multiple of 16) */
+  int had_p, had_m;          /* full-width Hadamard plan (Hadamard modes) */
+  const int8_t* had_base;    /* [had_m, had_m] host pointer */
+  int32_t* oacc;             /* [M, d_model] */
+} qmb_tp_args;
+int qmb_block_tp_stage(const qmb_block* blk, const qmb_tp_args* tp, const int8_t* u_q, double u_scale, int B,
+                       int T, int decode, int8_t* conv_state, float* ssm_state, float* out, int accumulate,
+                       void* ws, size_t ws_bytes, uint32_t* err_flag, qmb_stream_t stream);
+
 int qmb_block_prefill_profiled(const qmb_block* blk, const int8_t* u_q, double u_scale, int B, int T,
                                float* out, int scan_exp, void* workspace, size_t ws_bytes,
                                uint32_t* err_flag, qmb_stream_t stream, float stage_ms[QMB_NUM_STAGES]);

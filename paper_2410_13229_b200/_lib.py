@@ -43,6 +43,13 @@ class BlockDesc(ctypes.Structure):
     ]
 
 
+class TpArgs(ctypes.Structure):  # qmb_tp_args
+    _fields_ = [("stage", c_int), ("xacc", ctypes.c_void_p), ("y_local", ctypes.c_void_p),
+                ("y_full", ctypes.c_void_p), ("yq_full", ctypes.c_void_p), ("e_full", ctypes.c_longlong),
+                ("e0", c_int), ("had_p", c_int), ("had_m", c_int), ("had_base", ctypes.c_void_p),
+                ("oacc", ctypes.c_void_p)]
+
+
 # name -> (restype, argtypes); must match include/qmb.h exactly
 PROTOTYPES = {
     "qmb_abi_version": (c_int, []),
@@ -70,6 +77,8 @@ PROTOTYPES = {
     "qmb_selective_scan": (c_int, [c_i8p, c_dbl, c_i8p, c_dbl, c_i8p, c_dbl, c_i8p, c_dbl, c_i8p, c_dbl, c_i8p,
                                    c_dbl, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_vp, c_sz, c_vp, c_vp]),
     "qmb_selective_scan_workspace_bytes": (c_sz, [c_int, c_int]),
+    "qmb_block_tp_stage": (c_int, [c_vp, ctypes.POINTER(TpArgs), c_vp, c_dbl, c_int, c_int, c_int, c_vp, c_vp, c_vp,
+                                   c_int, c_vp, c_sz, c_vp, c_vp]),
     "qmb_hadamard_quantize": (c_int, [c_vp, c_ll, c_int, c_int, c_i8p, c_dbl, c_int, c_i8p, c_vp, c_vp, c_vp]),
     "qmb_measure_i8_peak": (c_int, [c_int, ctypes.POINTER(c_dbl)]),
     "qmb_gemm_bench": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(ctypes.c_float)]),

@@ -392,12 +392,78 @@ static thread_local cudaEvent_t* g_prof = nullptr;
     if (g_prof) cudaEventRecord(g_prof[(i)], (st));   \
   } while (0)
 
+// Tensor-parallel back half on an E-sharded handle (channels [e0, e0 + E) of the
+// full d_inner tp->e_full): stage 3 quantizes the gathered gated y [M, e_full]
+// (Hadamard with the FULL plan, qblock.py:211-214) and multiplies the local K-slice
+// of y_q with this handle's rows of w_out(_h), leaving exact int32 partial sums in
+// tp->oacc [M, D]; stage 4 applies out_proj's epilogue to the all-reduced sums
+// (extra scale 1 / e_full, qblock.py:213).  int32 sums are exact in any order, so
+// the result is bit-identical to the unsharded block.
+static int tp_back(const qmb_block* b, const qmb_tp_args* tp, int B, int T, float* out, bool accum, uint32_t* err,
+                   cudaStream_t st, int32_t* acc32, long long M) {
+  const int D = b->D, E = b->E;
+  const long long Ef = tp->e_full;
+  if (Ef % 16 || tp->e0 % 16 || tp->e0 + E > Ef) return fail(QMB_E_ARG, "tensor-parallel channel range is inconsistent");
+  if (tp->stage == 3) {
+    if (b->had) {
+      HadParams hp{};
+      hp.y = tp->y_full;
+      hp.ldy = Ef;
+      hp.out = tp->yq_full;
+      hp.ldo = Ef;
+      hp.yh = nullptr;
+      hp.M = M;
+      hp.p = tp->had_p;
+      hp.m = tp->had_m;
+      if ((hp.m != 1 && hp.m != 12 && hp.m != 20) || ((long long)hp.m << hp.p) != Ef)
+        return fail(QMB_E_ARG, "plan factorization is inconsistent");
+      for (int o = 0; o < hp.m; ++o) {
+        uint32_t row = 0;
+        for (int k = 0; k < hp.m; ++k) row |= (tp->had_base[o * hp.m + k] > 0 ? 1u : 0u) << k;
+        hp.base_rows[o] = row;
+      }
+      hp.s_out = f32(b->act[QMB_ACT_Y_HAD]);
+      hp.qmax = b->qmax;
+      hp.err = err;
+      QMB_CUDA(hadamard_quant(hp, st), "tp hadamard");
+    } else {
+      QMB_CUDA(quantize_f32_2d(tp->y_full, Ef, M, Ef, f32(b->act[QMB_ACT_Y]), b->qmax, tp->yq_full, Ef, err, st),
+               "tp y quantize");
+    }
+    EpiParams rp{};
+    rp.nseg = 1;
+    rp.qmax = b->qmax;
+    rp.err = err;
+    rp.seg[0] = EpiSeg{0, D, EPI_F32, 1.0f, 1.0f, nullptr, D, nullptr};
+    rp.raw_out = tp->oacc;
+    rp.raw_ld = D;
+    QMB_CUDA(gemm_i8(tp->yq_full + tp->e0, Ef, b->w_out_t, b->Ep, (int)M, D, E, rp, st, 0, acc32),
+             "tp out_proj partial gemm");
+    return 0;
+  }
+  EpiParams ep{};
+  ep.nseg = 1;
+  ep.qmax = b->qmax;
+  ep.err = err;
+  const double s_y = b->had ? b->act[QMB_ACT_Y_HAD] : b->act[QMB_ACT_Y];
+  const double extra = b->had ? 1.0 / (double)Ef : 1.0;
+  ep.seg[0] = EpiSeg{0, D, accum ? EPI_F32_ADDTO : EPI_F32, f32(s_y * b->s_w_out * extra), 1.0f, out, D, nullptr};
+  QMB_CUDA(epi_apply_i32(tp->oacc, (int)M, D, ep, st), "tp out_proj finish");
+  return 0;
+}
+
 // Shared body of prefill (T >= 1 per sequence, h0 = 0) and decode (T = 1 with
 // carried conv window and h).
 static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int B, int T, float* out, int8_t* conv_state,
                      float* ssm_state, bool decode, int8_t* conv_state_out, float* ssm_state_out, int scan_exp,
-                     void* ws, size_t ws_bytes, uint32_t* err, cudaStream_t st, bool accum = false) {
-  if (!b || !u_q || !out) return fail(QMB_E_ARG, "null argument");
+                     void* ws, size_t ws_bytes, uint32_t* err, cudaStream_t st, bool accum = false,
+                     const qmb_tp_args* tp = nullptr) {
+  // tensor-parallel stages (qmb_block_tp_stage): 1 = in_proj .. x_proj partial sums,
+  // 2 = x_proj finish .. gated y of the local channels, 3 = Hadamard of the gathered
+  // y + out_proj partial sums, 4 = out_proj finish
+  const int stage = tp ? tp->stage : 0;
+  if (tp && (stage < 1 || stage > 4)) return fail(QMB_E_ARG, "tensor-parallel stage must be 1..4");
+  if (!b || (!u_q && stage <= 1) || (!out && (stage == 0 || stage == 4))) return fail(QMB_E_ARG, "null argument");
   if (B < 0 || T < 0) return fail(QMB_E_ARG, "batch and length must be non-negative");
   const long long M = (long long)B * T;
   if (M == 0) return 0;
@@ -418,8 +484,13 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
   const int D = b->D, E = b->E, N = b->N, R = b->R;
   const double s_u = u_scale > 0.0 ? u_scale : b->act[QMB_ACT_IN];
 
+  if (stage >= 3) return tp_back(b, tp, B, T, out, accum, err, st, acc32, M);
+  bool fused_dscan = false;
+  int xsplit = 0;
+  EpiParams xepi{};
   // in_proj (qblock.py:192-198)
   PROF(0, st);
+  if (stage != 2) {
   const int8_t* A = u_q;
   long long lda = D;
   if ((D % 16) || ((uintptr_t)u_q % 16)) {
@@ -442,10 +513,11 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     ep.seg[1] = EpiSeg{E, 2 * E, zsilu_in_gemm() ? EPI_F32_SILU : EPI_F32, s_lin, 1.0f, z, E, nullptr};
     QMB_CUDA(gemm_i8(A, lda, b->w_in_t, b->Dp, (int)M, 2 * E, D, ep, st, 0, acc32), "in_proj gemm");
   }
+  }  // (stage != 2)
   // conv + SiLU + requant (qblock.py:199-201 -> fused_qconv :126-143)
   const float s_conv = f32(b->act[QMB_ACT_CONV_IN] * b->s_conv_w);
   PROF(1, st);
-  if (decode && b->exp_tab && zsilu_in_gemm() && decode_mid_enabled() &&
+  if (!tp && decode && b->exp_tab && zsilu_in_gemm() && decode_mid_enabled() &&
       (long long)decode_mid_grid(E) * B * b->Nx <= SPLITK_SCRATCH_INTS && decode_mid_ok(B, E, N, b->Kc, b->Nx, R, b->Rp)) {
     // conv step, x_proj, dt_proj + softplus, scan step and gate in one kernel
     DecodeMidParams dp{};
@@ -502,6 +574,18 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     PROF(3, st);
     PROF(4, st);
   } else {
+  if (stage == 2) {  // x_proj's requant from the all-reduced int32 sums
+    EpiParams ep{};
+    ep.nseg = 3;
+    ep.qmax = b->qmax;
+    ep.err = err;
+    const double s_x = b->act[QMB_ACT_X];
+    ep.seg[0] = EpiSeg{0, N, EPI_QUANT, f32(s_x * b->s_w_b * 1.0), f32(b->act[QMB_ACT_B]), bq, N, nullptr};
+    ep.seg[1] = EpiSeg{N, 2 * N, EPI_QUANT, f32(s_x * b->s_w_c * 1.0), f32(b->act[QMB_ACT_C]), cq, N, nullptr};
+    ep.seg[2] = EpiSeg{2 * N, 2 * N + R, EPI_QUANT, f32(s_x * b->s_w_dtr * 1.0), f32(b->act[QMB_ACT_DT_R]), dtr,
+                       b->Rp, nullptr};
+    QMB_CUDA(epi_apply_i32(tp->xacc, (int)M, b->Nx, ep, st), "x_proj finish");
+  } else {
   if (decode) {
     QMB_CUDA(conv_step(xq, E, conv_state, b->conv_w, b->conv_b, scanx, b->Ep, B, E, b->Kc, s_conv,
                        f32(b->act[QMB_ACT_X]), b->qmax, err, st),
@@ -527,9 +611,6 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
   }
   // x_proj: b, c, dt_r (qblock.py:202-204)
   PROF(2, st);
-  bool fused_dscan = false;
-  int xsplit = 0;
-  EpiParams xepi{};
   {
     EpiParams ep{};
     ep.nseg = 3;
@@ -543,14 +624,26 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     // (B <= 8: x_proj runs as the GEMV with its epilogue; at larger B the per-row finish
     // of x_proj's split-K partials inside the scan kernel measured slower than the
     // separate fix-up + dt_proj kernels: B = 64, 16 layers 1.73 vs 1.54 ms)
-    fused_dscan = decode && B <= 8 && b->exp_tab && zsilu_in_gemm() && decode_scan_enabled() &&
+    fused_dscan = !tp && decode && B <= 8 && b->exp_tab && zsilu_in_gemm() && decode_scan_enabled() &&
                   decode_scan_ok(B, E, N, b->Nx, R, b->Rp);
+    if (stage == 1) {  // K-sharded x_proj: the exact int32 partial sums, all-reduced by the caller
+      EpiParams rp{};
+      rp.nseg = 1;
+      rp.qmax = b->qmax;
+      rp.err = err;
+      rp.seg[0] = EpiSeg{0, b->Nx, EPI_F32, 1.0f, 1.0f, nullptr, b->Nx, nullptr};
+      rp.raw_out = tp->xacc;
+      rp.raw_ld = b->Nx;
+      QMB_CUDA(gemm_i8(scanx, b->Ep, b->w_x_t, b->Ep, (int)M, b->Nx, E, rp, st, 0, acc32), "x_proj partial gemm");
+      return 0;
+    }
     // fused decode scan: x_proj may leave its split-K partials for the scan kernel to finish
     QMB_CUDA(gemm_i8(scanx, b->Ep, b->w_x_t, b->Ep, (int)M, b->Nx, E, ep, st, 0, acc32,
                      fused_dscan ? &xsplit : nullptr),
              "x_proj gemm");
     xepi = ep;
   }
+  }  // (stage != 2: conv, x_proj)
   // dt_proj + bias + softplus + quantize (qblock.py:205-206)
   PROF(3, st);
   if (fused_dscan) {
@@ -641,6 +734,12 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     QMB_CUDA(selective_scan(sp, use_lut, st), "scan");
   }  // (unfused dt_proj + scan)
   }  // (unfused stages)
+  if (stage == 2) {  // the local channels' gated y, all-gathered by the caller
+    QMB_CUDA(cudaMemcpy2DAsync(tp->y_local, (size_t)E * 4, z, (size_t)E * 4, (size_t)E * 4, M,
+                               cudaMemcpyDeviceToDevice, st),
+             "tp y copy");
+    return 0;
+  }
   // output quantization (qblock.py:211-214)
   PROF(5, st);
   if (b->had) {
@@ -981,4 +1080,17 @@ extern "C" int qmb_embed_gather(const float* table, const long long* tokens, lon
                                 qmb_stream_t stream) {
   QMB_CUDA(embed_gather(table, tokens, n, D, out, (cudaStream_t)stream), "embed");
   return 0;
+}
+
+extern "C" int qmb_block_tp_stage(const qmb_block* b, const qmb_tp_args* tp, const int8_t* u_q, double u_scale, int B,
+                                  int T, int decode, int8_t* conv_state, float* ssm_state, float* out, int accumulate,
+                                  void* ws, size_t ws_bytes, uint32_t* err, qmb_stream_t stream) {
+  if (!tp) return fail(QMB_E_ARG, "null argument");
+  if (decode && T != 1) return fail(QMB_E_ARG, "decode advances one token per sequence");
+  if ((tp->stage == 1 && !tp->xacc) || (tp->stage == 2 && (!tp->xacc || !tp->y_local)) ||
+      (tp->stage == 3 && (!tp->y_full || !tp->yq_full || !tp->oacc)) || (tp->stage == 4 && !tp->oacc))
+    return fail(QMB_E_ARG, "null argument");
+  return block_run(b, u_q, u_scale, B, T, out, decode ? conv_state : nullptr, decode ? ssm_state : nullptr,
+                   decode != 0, decode ? nullptr : conv_state, decode ? nullptr : ssm_state, 0, ws, ws_bytes, err,
+                   (cudaStream_t)stream, accumulate != 0, tp);
 }

@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
       if (PF && part < CHUNKS) tmem_ld_32x32b_x32_nowait(tcol + part * 32, rn);
 #pragma unroll 1
       for (int c = part; c < CHUNKS; c += PARTS) {
-        if (SUB8 && splitk == 1) {
+        if (SUB8 && splitk == 1 && !ep.raw_out) {
           const int nb = n0 + c * 32;
           if (nb >= N) continue;
           int oc;
@@ -543,10 +543,11 @@ __global__ void __launch_bounds__(TcCfg<BN, EPIW, TMAOUT, CG>::THREADS, 1)
         }
         const int nb = n0 + c * 32;
         if (nb >= N) continue;  // warp-uniform
-        if (splitk > 1) {       // split-K partial -> acc32[split][M][N]; summed (exactly) afterwards
-          if (m < M) {
-            int32_t* dst = ep.acc32 + ((long long)(tile % splitk) * M + m) * N + nb;
-            if (nb + 32 <= N && (N % 4) == 0) {
+        if (splitk > 1 || ep.raw_out) {  // split-K partial -> acc32[split][M][N] (summed exactly afterwards),
+          if (m < M) {                   // or the raw int32 sums -> raw_out (tensor-parallel partials)
+            int32_t* dst = splitk > 1 ? ep.acc32 + ((long long)(tile % splitk) * M + m) * N + nb
+                                      : ep.raw_out + m * ep.raw_ld + nb;
+            if (nb + 32 <= N && (N % 4) == 0 && (splitk > 1 || ep.raw_ld % 4 == 0)) {
 #pragma unroll
               for (int j = 0; j < 32; j += 4)
                 *reinterpret_cast<int4*>(dst + j) = make_int4((int)r[j], (int)r[j + 1], (int)r[j + 2], (int)r[j + 3]);
@@ -1118,7 +1119,7 @@ static cudaError_t launch_tc_bn(const int8_t* A, long long lda, const int8_t* Bt
     const EpiSeg& g = ep.seg[s];
     // (silu(z) stays on 8 warps: measured faster than 16, whose register budget spills it)
     if (g.kind == EPI_SOFTPLUS_Q) heavy = true;
-    if (!tma_storable(g)) continue;
+    if (!tma_storable(g) || ep.raw_out) continue;
     if (ep.tma_seg < 0)
       ep.tma_seg = s;
     else if (ep.tma_seg2 < 0)
@@ -1304,6 +1305,23 @@ __global__ void epi_apply_kernel(const int32_t* __restrict__ acc, int splitk, in
 }
 
 
+
+// The epilogue of `ep` over exact int32 sums acc [M, N] (row stride N): the
+// tensor-parallel finish after an all-reduce of partial products.
+cudaError_t epi_apply_i32(const int32_t* acc, int M, int N, const EpiParams& ep_in, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  EpiParams ep = ep_in;
+  ep.splitk = 1;
+  ep.acc32 = nullptr;
+  ep.qtab_bias = QTAB_BIAS;
+  ep.one2 = kOne2;
+  ep.negz2 = kNegZero2;
+  for (int s = 0; s < ep.nseg; ++s) ep.seg[s].out_inv = 1.0f / ep.seg[s].out_div;  // RN f32 reciprocal
+  const long long total = (long long)M * N;
+  long long blocks = (total + 255) / 256;
+  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+  return launch_pdl(M <= 128, epi_apply_kernel, dim3((unsigned)blocks), dim3(256), 0, st, acc, 1, M, N, ep);
+}
 
 template <int BN>
 static cudaError_t launch_tc_choose(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N,

@@ -144,6 +144,8 @@ struct EpiParams {
   unsigned long long one2, negz2;  // packed {1, 1} / {-0, -0} as run-time operands (set by gemm_i8)
   int splitk;      // > 1: split-K over K blocks; partial int32 sums stored per split
   int32_t* acc32;  // [splitk, M, N] int32 partials; a second kernel sums them and runs the epilogue
+  int32_t* raw_out;  // non-null: the exact int32 sums go to raw_out[m * raw_ld + n] instead of any epilogue
+  long long raw_ld;  // (single segment [0, N), no interleave; tensor-parallel partial products)
 };
 
 // Segment by value with compile-time indices only: a runtime index into the
@@ -190,6 +192,10 @@ __device__ __forceinline__ const float* stage_qtab(const EpiParams& ep, float* d
 // null for the exact evaluation.
 __device__ __forceinline__ void epi_store_one(const EpiParams& ep, const EpiSeg& sg, long long m, int oc, int acc,
                                               uint32_t& err, const float* sqtab = nullptr) {
+  if (ep.raw_out) {  // raw mode: one segment [0, N), so oc is the GEMM column
+    ep.raw_out[m * ep.raw_ld + oc] = acc;
+    return;
+  }
   float v = __fmul_rn(__int2float_rn(acc), sg.acc_scale);
   if (sg.bias) v = __fadd_rn(v, sg.bias[oc]);
   long long off = m * sg.ld + oc;
@@ -217,6 +223,7 @@ constexpr long long SPLITK_SCRATCH_INTS = 148LL * 128 * 256;
 cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
                     const EpiParams& ep, cudaStream_t st, int force_path /*0 auto, 1 tc, 2 simt, 3 gemv*/,
                     int32_t* acc32_scratch = nullptr, int* defer_splitk = nullptr);
+cudaError_t epi_apply_i32(const int32_t* acc, int M, int N, const EpiParams& ep, cudaStream_t st);
 // defer_splitk (nullable): when the launch splits K (skinny M with acc32_scratch), skip
 // the fix-up kernel and return the split count here (the int32 partials are left in
 // acc32_scratch as [split][M][N] for the caller's next kernel); 0 = the epilogue ran.

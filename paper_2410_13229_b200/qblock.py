@@ -104,12 +104,13 @@ class DeviceBlock:
     """An uploaded QuantizedBlock: one libqmb handle (int8 weights repacked
     K-major, f32 epilogue constants, dequant and expf tables) living in HBM."""
 
-    def __init__(self, qb):
+    def __init__(self, qb, d_inner: int | None = None):
+        """d_inner: override for a channel slice of a block (tensor parallelism, tp.py)."""
         _device.device()
         lib = _lib.load()
         cfg = qb.cfg
         mode = _mode_value(qb.mode)
-        self.d_model, self.d_inner = int(cfg.d_model), int(cfg.d_inner)
+        self.d_model, self.d_inner = int(cfg.d_model), int(d_inner if d_inner is not None else cfg.d_inner)
         self.d_state, self.d_conv, self.dt_rank = int(cfg.d_state), int(cfg.d_conv), int(cfg.dt_rank)
         self.bit_width = int(qb.weights["w_in"].bit_width)
         self.act_in = float(qb.act["in"].scale)
