@@ -385,6 +385,25 @@ def run_ours(args):
         extras["long_context_4x16k"] = _prefill_line(dm, ltok, 2, stream, world, dev)
         del ltok
         torch.cuda.empty_cache()
+    if world > 1 and not args.no_extras:
+        # batch-1 latency over all N GPUs: tensor-parallel E-sharding --
+        # each rank streams 1/N of every block's weights; three collectives per layer
+        # (int32 all-reduces of the x_proj / out_proj partials, a gather of the gated y)
+        from paper_2410_13229_b200.tp import DistComm, TPModel
+
+        tpm = TPModel(qm, DistComm(), [rank], world)
+        tstates = tpm.new_states(1)
+        tpm.prefill(tokens[:1, :16].contiguous(), tstates)
+        cur = tokens[:1, 0].contiguous()
+        for _ in range(3):
+            tpm.decode_step(cur, tstates)
+        ms_tp = _timed(lambda: tpm.decode_step(cur, tstates), max(10, args.steps * 4), stream, world, dev)
+        extras["tp_batch1_decode"] = {
+            "value": 1.0 / (ms_tp * 1e-3), "unit": "tokens/s", "batch": 1, "tensor_parallel": world,
+            "ms_per_token": ms_tp,
+            "note": "one sequence served by all N GPUs (channel-sharded blocks, eager, %s collectives)" % backend}
+        del tpm, tstates
+        torch.cuda.empty_cache()
 
     # ---------------------------------------------------------- roofline of the dominant kernel
     import ctypes

@@ -45,7 +45,8 @@ def shard_block(qb, rank: int, world: int):
     El = E // world
     e0 = rank * El
     sl = slice(e0, e0 + El)
-    W = {k: np.asarray(v.values) for k, v in qb.weights.items()}
+    W = {k: (v.values.detach().cpu().numpy() if isinstance(v.values, torch.Tensor) else np.asarray(v.values))
+         for k, v in qb.weights.items()}
     parts = {
         "w_in": np.concatenate([W["w_in"][:, sl], W["w_in"][:, E + e0:E + e0 + El]], axis=1),
         "conv_w": W["conv_w"][:, sl], "conv_b": W["conv_b"][sl], "a": W["a"][sl], "d": W["d"][sl],
@@ -162,3 +163,65 @@ def tp_block_forward(shards: list, comm, u_q, B: int, T: int, outs: list, *, dec
     for s, b, o in zip(shards, bufs, outs):
         s.stage(4, b, None, B, T, out=o, accumulate=accumulate)
     return outs
+
+
+class TPModel:
+    """The quantized model loop (model.py:246-258) over tensor-parallel blocks:
+    embedding, norms and LM head replicated, each block split into channel shards.
+    `shard_ids`: the shards this process holds -- [rank] with DistComm, all of
+    range(world) with VirtualComm.  Bit-identical to DeviceModel."""
+
+    def __init__(self, model, comm, shard_ids: list, world: int):
+        from .model import DeviceModel
+
+        self.comm, self.world, self.ids = comm, world, list(shard_ids)
+        base = DeviceModel.__new__(DeviceModel)  # embedding / norm / LM-head helpers only
+        cfg = model.config
+        base.cfg, base.D, base.V, base.bits = cfg, int(cfg.d_model), int(cfg.vocab_size), int(cfg.bit_width)
+        from .model import _f32_dev
+
+        base.embedding = _f32_dev(model.embedding)
+        base.final_norm = _f32_dev(model.final_norm)
+        base.norms = [_f32_dev(l.norm_weight) for l in model.layers]
+        base.s_in = [float(l.block.act["in"].scale) for l in model.layers]
+        base.gains_finite = all(bool(torch.isfinite(g).all()) for g in base.norms + [base.final_norm])
+        base._lib = _lib.load()
+        self.base = base
+        self.layers = [[TPBlock(l.block, r, world) for r in self.ids] for l in model.layers]
+
+    def new_states(self, B: int):
+        return [[s.new_state(B) for s in shards] for shards in self.layers]
+
+    def _run(self, tokens: torch.Tensor, B: int, T: int, states, decode: bool):
+        M = B * T
+        base, stream, err = self.base, _device.stream_ptr(), _device.err_flag()
+        x_out = base.embed(tokens)
+        res = [torch.zeros_like(x_out) for _ in self.ids]
+        u_q = torch.empty((M, base.D), dtype=torch.int8, device=x_out.device)
+        bufs = [s.buffers(M) for s in self.layers[0]]
+        for li, shards in enumerate(self.layers):
+            if li == 0:
+                base._rmsnorm(x_out, res[0], res[0], base.norms[li], base.s_in[li], u_q, None, M, err, stream)
+                for r in res[1:]:
+                    r.copy_(res[0])
+            else:
+                base._rmsnorm(res[0], None, None, base.norms[li], base.s_in[li], u_q, None, M, err, stream)
+            tp_block_forward(shards, self.comm, u_q, B, T, res, decode=decode,
+                             states=states[li] if states is not None else None, accumulate=True, bufs=bufs)
+        final = torch.empty_like(x_out)
+        base._rmsnorm(res[0], None, None, base.final_norm, 1.0, None, final, M, err, stream)
+        return final
+
+    def forward_hidden(self, tokens: torch.Tensor, states=None) -> torch.Tensor:
+        B, T = tokens.shape
+        return self._run(tokens, B, T, states, False)
+
+    def prefill(self, tokens: torch.Tensor, states=None):
+        B, T = tokens.shape
+        states = states if states is not None else self.new_states(B)
+        final = self._run(tokens, B, T, states, False)
+        return self.base.lm_head(final.reshape(B, T, self.base.D)[:, -1]), states
+
+    def decode_step(self, tokens: torch.Tensor, states) -> torch.Tensor:
+        B = tokens.shape[0]
+        return self.base.lm_head(self._run(tokens, B, 1, states, True))

@@ -71,3 +71,34 @@ def test_tp_block_two_processes_gloo(cuda):
                        cwd=str(here.parent))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("tp rank ok") == 2, r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_tp_model_bit_exact(cuda, G):
+    """The whole model loop over TP blocks (config1: d_model 256, 4 layers):
+    hidden states of a prefill and the logits of carried-state decode steps equal
+    DeviceModel's bit for bit."""
+    from conftest import load_npz
+    from fixtures_util import mirror_model
+
+    from paper_2410_13229_b200.model import device_model
+    from paper_2410_13229_b200.tp import TPModel, VirtualComm
+
+    z, meta = load_npz("model_config1.npz")
+    qm = mirror_model(z, meta)
+    dm = device_model(qm)
+    tp = TPModel(qm, VirtualComm(G), list(range(G)), G)
+    tok = torch.from_numpy(z["tokens"][None, :64].astype(np.int64)).cuda().repeat(2, 1)
+    want_h = dm.forward_hidden(tok)
+    got_h = tp.forward_hidden(tok)
+    assert np.array_equal(_bits(got_h), _bits(want_h))
+    s_ref = dm.new_states(2)
+    dm.prefill(tok, s_ref)
+    s_tp = tp.new_states(2)
+    tp.prefill(tok, s_tp)
+    cur = tok[:, -1].contiguous()
+    for _ in range(3):
+        a = dm.decode_step(cur, s_ref)
+        b = tp.decode_step(cur, s_tp)
+        assert np.array_equal(_bits(a), _bits(b))
+        cur = a.argmax(-1)
