@@ -323,7 +323,7 @@ static void ws_layout(const qmb_block* b, long long M, size_t off[QMB_WS_COUNT],
   off[QMB_WS_DELTA] = take((size_t)M * b->E);
   off[QMB_WS_YQ] = take((size_t)M * b->Ep);
   off[QMB_WS_BCF] = take((size_t)M * 36 * 4);  // BCF_LD-float rows (scan staging pitch)
-  off[QMB_WS_ACC32] = take(M <= 128 ? (size_t)SPLITK_SCRATCH_INTS * 4 : 0);
+  off[QMB_WS_ACC32] = take(M <= 4096 ? (size_t)SPLITK_SCRATCH_INTS * 4 : 0);  // split-K scratch (skinny GEMMs)
   *total = o;
 }
 
@@ -480,7 +480,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
   int8_t* delta = (int8_t*)(w + off[QMB_WS_DELTA]);
   int8_t* yq = (int8_t*)(w + off[QMB_WS_YQ]);
   float* bcf = (float*)(w + off[QMB_WS_BCF]);
-  int32_t* acc32 = M <= 128 ? (int32_t*)(w + off[QMB_WS_ACC32]) : nullptr;
+  int32_t* acc32 = M <= 4096 ? (int32_t*)(w + off[QMB_WS_ACC32]) : nullptr;
   const int D = b->D, E = b->E, N = b->N, R = b->R;
   const double s_u = u_scale > 0.0 ? u_scale : b->act[QMB_ACT_IN];
 
@@ -886,7 +886,7 @@ extern "C" size_t qmb_qlinear_workspace_bytes(long long M, int K, int N) {
   const long long Kp = round_up(K, 16);
   // + split-K scratch for decode-size M
   return (size_t)(round_up(M * Kp, 256) + round_up((long long)N * Kp, 256) + round_up((long long)N * 4, 256) +
-                  (M <= 64 ? SPLITK_SCRATCH_INTS * 4 : 0));
+                  (M <= 4096 ? SPLITK_SCRATCH_INTS * 4 : 0));
 }
 
 extern "C" int qmb_qlinear(const int8_t* x_q, long long M, int K, double s_x, const int8_t* w_q, int N, double s_w,
@@ -925,7 +925,7 @@ extern "C" int qmb_qlinear(const int8_t* x_q, long long M, int K, double s_x, co
   else
     ep.seg[0] = EpiSeg{0, N, EPI_F32, acc_scale, 1.0f, out, N, bias_q ? bias : nullptr};
   int32_t* acc32 = nullptr;
-  if (M <= 64)  // split-K scratch for decode-size M
+  if (M <= 4096)  // split-K scratch (skinny products)
     acc32 = (int32_t*)(w + round_up(M * Kp, 256) + round_up((long long)N * Kp, 256) + round_up((long long)N * 4, 256));
   QMB_CUDA(gemm_i8(A, lda, bt, Kp, (int)M, N, K, ep, st, path, acc32), "qlinear gemm");
   return 0;

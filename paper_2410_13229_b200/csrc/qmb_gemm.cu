@@ -1332,6 +1332,7 @@ static cudaError_t launch_tc_choose(const int8_t* A, long long lda, const int8_t
   if (acc32 && tiles * 2 <= num_sms() && num_k > 1) {
     splitk = num_sms() / tiles;
     if (splitk > num_k) splitk = num_k;
+    while (splitk > 1 && (long long)splitk * M * N > SPLITK_SCRATCH_INTS) --splitk;  // partials fit the scratch
     const int kper = (num_k + splitk - 1) / splitk;  // no empty splits
     splitk = (num_k + kper - 1) / kper;
   }
@@ -1398,7 +1399,9 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
   if (path == 0) path = (tc_ok && (M > 16 || acc32)) ? 1 : 2;
   if (path == 1 && !tc_ok) return cudaErrorInvalidValue;
   if (path == 1) {
-    if (M > TC_BM) acc32 = nullptr;  // split-K only for skinny (decode-like) M
+    // split-K when there are too few output tiles to keep the SMs streaming (decode;
+    // x_proj / out_proj of a short prefill), as far as the partials fit the scratch
+    if ((long long)M * N * 2 > SPLITK_SCRATCH_INTS) acc32 = nullptr;
     // skinny M: one wave of 96-column tiles beats two waves of 64-column ones
     if (M <= TC_BM && N > 192 && (N + 63) / 64 > num_sms() && (N + 95) / 96 <= num_sms())
       return launch_tc_choose<96>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
