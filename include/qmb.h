@@ -256,6 +256,10 @@ int qmb_measure_i8_peak(int iters, double* tops);
 int qmb_gemm_bench(int M, int N, int K, int mode, int iters, float* ms);
 
 /* Embedding row gather (model.py:249): out[r] = table[tokens[r]]. */
+/* The tied f32 LM head final @ embedding^T (model.py:257-258): x [M, K], emb [V, K]
+ * -> out [M, V] f32.  Tolerance-only (the reference's BLAS sums in its own order). */
+int qmb_lm_head(const float* x, int M, int K, const float* emb, int V, float* out, qmb_stream_t stream);
+
 int qmb_embed_gather(const float* table, const long long* tokens, long long n, int D, float* out,
                      qmb_stream_t stream);
 

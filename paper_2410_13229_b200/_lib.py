@@ -85,6 +85,7 @@ PROTOTYPES = {
     "qmb_eval_math":(c_int, [c_int, c_vp, c_vp, c_ll, c_vp]),
     "qmb_verify_math":(c_int, [c_int, c_int, c_vp, c_vp, c_vp]),
     "qmb_embed_gather": (c_int, [c_vp, c_vp, c_ll, c_int, c_vp, c_vp]),
+    "qmb_lm_head": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_vp, c_vp]),
 }
 
 _lib = None

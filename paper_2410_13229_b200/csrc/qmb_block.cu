@@ -812,6 +812,7 @@ extern "C" int qmb_block_prefill_accum(const qmb_block* b, const int8_t* u_q, do
 extern "C" int qmb_block_decode_accum(const qmb_block* b, const int8_t* u_q, double u_scale, int B,
                                       int8_t* conv_state, float* ssm_state, float* res, void* ws, size_t ws_bytes,
                                       uint32_t* err, qmb_stream_t stream) {
+  if (B == 0) return 0;  // (zero sequences: nothing to advance, like the reference's empty arrays)
   if (!conv_state || !ssm_state) return fail(QMB_E_ARG, "decode requires conv and ssm state");
   return block_run(b, u_q, u_scale, B, 1, res, conv_state, ssm_state, true, nullptr, nullptr, 0, ws, ws_bytes, err,
                    (cudaStream_t)stream, true);
@@ -820,6 +821,7 @@ extern "C" int qmb_block_decode_accum(const qmb_block* b, const int8_t* u_q, dou
 extern "C" int qmb_block_decode(const qmb_block* b, const int8_t* u_q, double u_scale, int B, int8_t* conv_state,
                                 float* ssm_state, float* out, void* ws, size_t ws_bytes, uint32_t* err,
                                 qmb_stream_t stream) {
+  if (B == 0) return 0;  // (zero sequences: nothing to advance, like the reference's empty arrays)
   if (!conv_state || !ssm_state) return fail(QMB_E_ARG, "decode requires conv and ssm state");
   return block_run(b, u_q, u_scale, B, 1, out, conv_state, ssm_state, true, nullptr, nullptr, 0, ws, ws_bytes, err,
                    (cudaStream_t)stream);
@@ -1093,4 +1095,10 @@ extern "C" int qmb_block_tp_stage(const qmb_block* b, const qmb_tp_args* tp, con
   return block_run(b, u_q, u_scale, B, T, out, decode ? conv_state : nullptr, decode ? ssm_state : nullptr,
                    decode != 0, decode ? nullptr : conv_state, decode ? nullptr : ssm_state, 0, ws, ws_bytes, err,
                    (cudaStream_t)stream, accumulate != 0, tp);
+}
+
+extern "C" int qmb_lm_head(const float* x, int M, int K, const float* emb, int V, float* out, qmb_stream_t stream) {
+  if (M < 0 || K <= 0 || V < 0 || (M && (!x || !emb || !out))) return fail(QMB_E_ARG, "null argument");
+  QMB_CUDA(lm_head(x, M, K, emb, V, out, (cudaStream_t)stream), "lm head");
+  return 0;
 }

@@ -1306,6 +1306,53 @@ __global__ void epi_apply_kernel(const int32_t* __restrict__ acc, int splitk, in
 
 
 
+// Split-K fix-up for many splits (decode x_proj: 40): 8 threads per output element,
+// each summing every 8th split with independent loads (one round trip), then the
+// eight partial sums through shared memory -- int32, exact in any order.
+constexpr int EPW_T = 256, EPW_G = 8;
+__global__ void __launch_bounds__(EPW_T) epi_apply_wide_kernel(const int32_t* __restrict__ acc, int splitk, int M,
+                                                               int N, EpiParams ep) {
+  __shared__ float sQt[QTAB_FLOATS];
+  __shared__ int sPart[EPW_G][EPW_T / EPW_G];
+  const float* qt = stage_qtab(ep, sQt);
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  uint32_t err = 0;
+  const long long total = (long long)M * N;
+  const int g = threadIdx.x / (EPW_T / EPW_G), e = threadIdx.x % (EPW_T / EPW_G);
+  for (long long base = (long long)blockIdx.x * (EPW_T / EPW_G); base < total;
+       base += (long long)gridDim.x * (EPW_T / EPW_G)) {
+    const long long k = base + e;
+    int s = 0;
+    if (k < total) {
+      int v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int sk = g + u * EPW_G;
+        v[u] = sk < splitk ? __ldg(acc + sk * total + k) : 0;
+      }
+      for (int sk = g + 8 * EPW_G; sk < splitk; sk += EPW_G) s += __ldg(acc + sk * total + k);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    sPart[g][e] = s;
+    __syncthreads();
+    if (g == 0 && k < total) {
+      int t = 0;
+#pragma unroll
+      for (int u = 0; u < EPW_G; ++u) t += sPart[u][e];
+      const long long m = k / N;
+      const int n = (int)(k - m * N);
+      int oc;
+      const EpiSeg sg = pick_seg(ep, epi_locate(ep, n, &oc));
+      epi_store_one(ep, sg, m, oc, t, err, qt);
+    }
+    __syncthreads();
+  }
+  flag_error(ep.err, err);
+}
+
 // The epilogue of `ep` over exact int32 sums acc [M, N] (row stride N): the
 // tensor-parallel finish after an all-reduce of partial products.
 cudaError_t epi_apply_i32(const int32_t* acc, int M, int N, const EpiParams& ep_in, cudaStream_t st) {
@@ -1352,6 +1399,12 @@ static cudaError_t launch_tc_choose(const int8_t* A, long long lda, const int8_t
   }
   ep.splitk = 1;
   const long long total = (long long)M * N;
+  if (splitk >= 2 * EPW_G) {  // many splits: 8 threads per output (one load round trip)
+    long long blocks = (total + EPW_T / EPW_G - 1) / (EPW_T / EPW_G);
+    if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+    return launch_pdl(true, epi_apply_wide_kernel, dim3((unsigned)blocks), dim3(EPW_T), 0, st,
+                      (const int32_t*)acc32, splitk, M, N, ep);
+  }
   long long blocks = (total + 255) / 256;
   if (blocks > num_sms() * 8) blocks = num_sms() * 8;
   return launch_pdl(true, epi_apply_kernel, dim3((unsigned)blocks), dim3(256), 0, st, (const int32_t*)acc32, splitk, M,

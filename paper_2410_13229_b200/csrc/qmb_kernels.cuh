@@ -174,6 +174,9 @@ struct DecodeScanParams {
 bool decode_scan_ok(int B, int E, int N, int Nx, int R, long long ld_wdt);
 cudaError_t decode_scan(const DecodeScanParams& p, cudaStream_t st);
 
+// Tied LM head: out[M, V] = x[M, K] @ emb[V, K]^T, f32 (FFMA2 register-blocked GEMM).
+cudaError_t lm_head(const float* x, int M, int K, const float* emb, int V, float* out, cudaStream_t st);
+
 // Verified softplus+quantize threshold table (QTAB_FLOATS floats at `tab`);
 // scratch2: 2 device uint32 words.  Enqueued on `st` (the sweep covers all 2^32 floats).
 cudaError_t build_softplus_qtab(float s_div, int qmax, float* tab, uint32_t* scratch2, cudaStream_t st);

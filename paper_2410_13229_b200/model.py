@@ -2,8 +2,8 @@
 plus the batched, state-carrying prefill/decode engine the B200 path adds.
 
 The per-layer work (fused residual+RMSNorm+quant, block forward) runs in
-libqmb; the tied f32 LM head is a plain f32 GEMM (cuBLAS through torch, TF32
-off) and is tolerance-checked only.
+libqmb; the tied f32 LM head (libqmb's GEMV up to 8 rows, cuBLAS f32 above)
+is tolerance-checked only.
 """
 from __future__ import annotations
 
@@ -108,6 +108,18 @@ class DeviceModel:
         return out
 
     def lm_head(self, final: torch.Tensor) -> torch.Tensor:
+        """Tied f32 logits final @ embedding^T (model.py:257-258); tolerance-only
+        against the reference's BLAS summation order.  Up to 8 rows: libqmb's
+        streaming f32 GEMV (the embedding read once); more rows: cuBLAS's f32 GEMM
+        (TF32 off) -- libqmb's FFMA2 tile kernel (qmb_lm_head) measured slower there
+        (B = 64: 464 vs 367 us), an f32 GEMM needs the tensor cores to do better."""
+        x = final.reshape(-1, self.D).contiguous()
+        M = x.shape[0]
+        if M <= 8:
+            out = torch.empty((M, self.V), dtype=torch.float32, device=x.device)
+            _lib.check(self._lib.qmb_lm_head(x.data_ptr(), int(M), self.D, self.embedding.data_ptr(), self.V,
+                                             out.data_ptr(), _device.stream_ptr()), "lm_head")
+            return out.reshape(tuple(final.shape[:-1]) + (self.V,))
         prev = torch.backends.cuda.matmul.allow_tf32
         torch.backends.cuda.matmul.allow_tf32 = False
         try:

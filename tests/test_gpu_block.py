@@ -266,3 +266,30 @@ def test_nonfinite_gain_raises(cuda):
     g[5] = np.nan
     with pytest.raises(ValueError, match="non-finite activation"):
         fused_rmsnorm_quant(x, np.zeros_like(x), g, 0.05)
+
+
+def test_block_empty_and_single_token_edges(cuda, oracle):
+    """Empty inputs (B = 0, T = 0) are no-ops like the reference's zero-length
+    arrays; T = 1 prefill equals the reference's one-row block (conv window of
+    zeros, h0 = 0); a 0-sequence decode is a no-op."""
+    from paper_2410_13229_b200 import QTensor, block_forward_q
+    from paper_2410_13229_b200.qblock import device_block
+
+    z, meta = load_block("m20_full")
+    w = block_weights(z, meta)
+    qb = mirror_block(z, meta, w)
+    ob = oracle_block(z, meta, w)
+    dev = device_block(qb)
+    D = meta["cfg"]["d_model"]
+    for B, T in ((0, 5), (3, 0)):
+        out = torch.full((max(B * T, 1), D), 7.0, device="cuda")
+        dev.prefill(torch.zeros((max(B * T, 1), D), dtype=torch.int8, device="cuda"), B, T, out,
+                    u_scale=meta["u_scale"])
+        assert bool((out == 7.0).all())
+    one = block_forward_q(QTensor(z["u_q"][:1], meta["u_scale"]), qb)
+    assert np.array_equal(one.view(np.uint32), oracle.block_forward_q(z["u_q"][:1], meta["u_scale"], ob).view(np.uint32))
+    conv, h = dev.new_state(1)
+    row = torch.full((1, D), 3.0, device="cuda")
+    dev.decode(torch.zeros((1, D), dtype=torch.int8, device="cuda")[:0], conv[:0], h[:0], row[:0],
+               u_scale=meta["u_scale"])
+    assert bool((row == 3.0).all())

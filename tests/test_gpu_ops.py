@@ -267,3 +267,19 @@ def test_rmsnorm_residual_quant_bit_exact(cuda, oracle, M, D):
     # test_qblock.py:187-192: cancellation gives exact zeros
     q, res = fused_rmsnorm_quant(x_out, -x_out, gain, 0.05)
     assert not q.values.any() and not res.any()
+
+
+@pytest.mark.parametrize("M,K,V", [(1, 2560, 50280), (64, 2560, 50280), (3, 768, 1000), (65, 100, 130), (7, 37, 5)])
+def test_lm_head_tolerance(cuda, M, K, V):
+    """The tied f32 LM head (model.py:257-258) against an f64 product: within the
+    logit tolerance of SURVEY §8c (1e-5 of the largest |logit|)."""
+    from paper_2410_13229_b200 import _device, _lib
+
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + V)
+    x = torch.randn((M, K), generator=g, device="cuda")
+    emb = torch.randn((V, K), generator=g, device="cuda") * 0.05
+    out = torch.empty((M, V), dtype=torch.float32, device="cuda")
+    _lib.call("qmb_lm_head", x.data_ptr(), M, K, emb.data_ptr(), V, out.data_ptr(), _device.stream_ptr())
+    ref = (x.double() @ emb.double().T)
+    err = float((out.double() - ref).abs().max())
+    assert err <= 1e-5 * float(ref.abs().max()), err
