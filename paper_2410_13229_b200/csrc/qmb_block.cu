@@ -486,8 +486,6 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
 
   if (stage >= 3) return tp_back(b, tp, B, T, out, accum, err, st, acc32, M);
   bool fused_dscan = false;
-  int xsplit = 0;
-  EpiParams xepi{};
   // in_proj (qblock.py:192-198)
   PROF(0, st);
   if (stage != 2) {
@@ -621,10 +619,10 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     ep.seg[1] = EpiSeg{N, 2 * N, EPI_QUANT, f32(s_x * b->s_w_c * 1.0), f32(b->act[QMB_ACT_C]), cq, N, nullptr};
     ep.seg[2] = EpiSeg{2 * N, 2 * N + R, EPI_QUANT, f32(s_x * b->s_w_dtr * 1.0), f32(b->act[QMB_ACT_DT_R]), dtr,
                        b->Rp, nullptr};
-    // (B <= 8: x_proj runs as the GEMV with its epilogue; at larger B the per-row finish
-    // of x_proj's split-K partials inside the scan kernel measured slower than the
-    // separate fix-up + dt_proj kernels: B = 64, 16 layers 1.73 vs 1.54 ms)
-    fused_dscan = !tp && decode && B <= 8 && b->exp_tab && zsilu_in_gemm() && decode_scan_enabled() &&
+    // decode below 16 sequences: dt_proj + softplus fused into the scan step kernel
+    // (16 layers at B = 8: 1.34 vs 1.49 ms; B = 1: 0.62 vs 0.66 ms).  From B = 16 the
+    // dt_proj GEMM + batch-tiled scan_tab16 is faster (B = 64: 1.49 vs 1.55 ms).
+    fused_dscan = !tp && decode && B < 16 && b->exp_tab && zsilu_in_gemm() && decode_scan_enabled() &&
                   decode_scan_ok(B, E, N, b->Nx, R, b->Rp);
     if (stage == 1) {  // K-sharded x_proj: the exact int32 partial sums, all-reduced by the caller
       EpiParams rp{};
@@ -637,26 +635,17 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
       QMB_CUDA(gemm_i8(scanx, b->Ep, b->w_x_t, b->Ep, (int)M, b->Nx, E, rp, st, 0, acc32), "x_proj partial gemm");
       return 0;
     }
-    // fused decode scan: x_proj may leave its split-K partials for the scan kernel to finish
-    QMB_CUDA(gemm_i8(scanx, b->Ep, b->w_x_t, b->Ep, (int)M, b->Nx, E, ep, st, 0, acc32,
-                     fused_dscan ? &xsplit : nullptr),
-             "x_proj gemm");
-    xepi = ep;
+    QMB_CUDA(gemm_i8(scanx, b->Ep, b->w_x_t, b->Ep, (int)M, b->Nx, E, ep, st, 0, acc32), "x_proj gemm");
   }
   }  // (stage != 2: conv, x_proj)
   // dt_proj + bias + softplus + quantize (qblock.py:205-206)
   PROF(3, st);
   if (fused_dscan) {
-    // dt_proj, softplus, the scan step and the gate in one kernel (+ the x_proj finish)
+    // dt_proj, softplus, the scan step and the gate in one kernel
     DecodeScanParams dp{};
     dp.x = scanx;
     dp.ldx = b->Ep;
     dp.z = z;
-    dp.splitk = xsplit;
-    dp.xpart = acc32;
-    dp.Nx = b->Nx;
-    dp.epx = xepi;
-    for (int k = 0; k < 3; ++k) dp.epx.seg[k].out_inv = 1.0f / dp.epx.seg[k].out_div;  // RN f32 reciprocal
     dp.bq = bq;
     dp.cq = cq;
     dp.dtr = dtr;

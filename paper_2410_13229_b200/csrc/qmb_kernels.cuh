@@ -153,16 +153,12 @@ bool decode_mid_ok(int B, int E, int N, int Kc, int Nx, int R, int Rp);
 int decode_mid_grid(int E);  // CTAs (= partial rows of xpart)
 cudaError_t decode_mid(const DecodeMidParams& p, cudaStream_t st);
 
-// Decode scan with dt_proj (and the x_proj finish when x_proj left split-K partials):
-// see decode_scan_kernel.
+// Decode scan with dt_proj fused (x_proj's b | c | dt_r codes as input): see
+// decode_scan_kernel.
 struct DecodeScanParams {
   const int8_t* x; long long ldx;     // [B, ldx] conv output (scan input) codes
   float* z;                           // [B, E] silu(z) in, gated y out
-  int splitk;                         // > 0: x_proj int32 partials [splitk][B][Nx] in xpart
-  const int32_t* xpart;
-  int Nx;
-  EpiParams epx;                      // x_proj epilogue (b | c | dt_r requant)
-  const int8_t* bq; const int8_t* cq; const int8_t* dtr; long long ld_dtr;  // splitk == 0: x_proj outputs
+  const int8_t* bq; const int8_t* cq; const int8_t* dtr; long long ld_dtr;  // x_proj outputs
   const int8_t* w_dt; long long ld_wdt; int R;  // [E, ld_wdt] dt_proj weights (K-major)
   float dt_scale; const float* dt_bias; const float* qtab; float dt_div, dt_inv;
   const float* lut_x; const float* lut_dt; const float* lut_b; const float* lut_c;
