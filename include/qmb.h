@@ -120,7 +120,10 @@ int qmb_block_workspace_layout(const qmb_block* blk, long long rows, size_t offs
  * out [B*T, d_model] f32.  Optional state outputs for the
  * decode handoff: conv_state_out [B, d_conv-1, d_inner] int8 (last x_q rows),
  * ssm_state_out [B, d_inner, d_state] f32 (final h of scan_core, kernels.py:99).
- * scan_exp: 0 = tabulated exact expf (default), 1 = direct FP64 restatement. */
+ * scan_exp: 0 = tabulated exact expf (default), 1 = direct FP64 restatement,
+ *   2 = fast mode: approximate exp (MUFU ex2) and contracted FMAs in the
+ *   batch-tiled prefill scan (B >= 16), NOT bit-exact -- y within a stated tolerance
+ *   of the exact scan; smaller batches and decode run exact. */
 int qmb_block_prefill(const qmb_block* blk, const int8_t* u_q, double u_scale, int B, int T, float* out,
                       int8_t* conv_state_out, float* ssm_state_out, int scan_exp,
                       void* workspace, size_t ws_bytes, uint32_t* err_flag, qmb_stream_t stream);

@@ -718,8 +718,10 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     sp.N = N;
     sp.err = err;
     // 1: tabulated expf in shared memory (prefill), 2: tabulated expf through L1
-    // (decode, one step per sequence), 0: direct FP64 glibc-expf restatement
-    const int use_lut = scan_exp != 0 ? 0 : (decode ? decode_scan_mode() : 1);
+    // (decode, one step per sequence), 0: direct FP64 glibc-expf restatement;
+    // scan_exp 2 = fast mode (approximate exp in the batch-tiled prefill kernel)
+    sp.fast = (scan_exp == 2 && !decode) ? 1 : 0;
+    const int use_lut = scan_exp == 1 ? 0 : (decode ? decode_scan_mode() : 1);
     QMB_CUDA(selective_scan(sp, use_lut, st), "scan");
   }  // (unfused dt_proj + scan)
   }  // (unfused stages)

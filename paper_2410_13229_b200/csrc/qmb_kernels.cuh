@@ -100,6 +100,8 @@ struct ScanParams {
   // f32(f64(q) * s) for every q in [-128, 127] (deq_split in qmb_block.cu)
   float dq_x_hi, dq_x_lo, dq_dt_hi, dq_dt_lo;
   int dq_fast;
+  int fast;                           // scan_exp = 2: approximate exp (MUFU ex2) in the batch-tiled
+                                      // kernel, not bit-exact (B < 16 and decode stay exact)
   float* h;                           // [B, E, N] carried state (in if h_in, out if h_out)
   int h_in, h_out;
   int B, T, E, N;

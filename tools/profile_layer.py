@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--seq", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--scan-exp", type=int, default=0, help="0 exact (default), 2 fast mode")
     args = ap.parse_args()
     import torch
 
@@ -51,8 +52,8 @@ def main():
     ms = (ctypes.c_float * 7)()
     acc = [0.0] * 7
     for r in range(args.reps + 1):
-        _lib.check(lib.qmb_block_prefill_profiled(blk.handle, u.data_ptr(), 0.0, B, T, out.data_ptr(), 0,
-                                                  ws.data_ptr(), ws.numel(), _device.err_flag().ptr,
+        _lib.check(lib.qmb_block_prefill_profiled(blk.handle, u.data_ptr(), 0.0, B, T, out.data_ptr(),
+                                                  args.scan_exp, ws.data_ptr(), ws.numel(), _device.err_flag().ptr,
                                                   torch.cuda.current_stream().cuda_stream, ms))
         if r:
             acc = [a + m / args.reps for a, m in zip(acc, ms)]
