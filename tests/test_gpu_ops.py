@@ -185,7 +185,21 @@ def test_hadamard_golden_and_quant(cuda, oracle):
     assert hadamard_quantize(np.array([[64.0, 0, 0, 0]], np.float32), 1.0, plan).values.tolist() == [[64] * 4]
 
 
-@pytest.mark.parametrize("n", [1536, 5120])
+@pytest.mark.parametrize("n", [1024, 2048, 3072, 4096])
+def test_hadamard_family_dims_bit_exact(cuda, oracle, n):
+    """The packed kernels at the other Mamba d_inner sizes (2^10..2^12 run the
+    butterfly alone, hadamard.py:145; 3072 = 12 x 2^8) against the oracle, which
+    the n = 512 / 16 / 96 / 1536 / 5120 goldens pin to the reference."""
+    from paper_2410_13229_b200 import apply_hadamard, plan_for_dim
+
+    plan = plan_for_dim(n)
+    y = (np.random.default_rng(n).standard_normal((9, n)) * 3).astype(np.float32)
+    y[1, ::5] = -0.0
+    got = apply_hadamard(plan, y)
+    assert _bits_equal(got, oracle.hadamard(y, plan.p, plan.m, plan.base)), n
+
+
+@pytest.mark.parametrize("n", [1536, 5120, 3072, 2048, 4096])
 def test_hadamard_quant_ties_clamps_and_nonfinite(cuda, oracle, n):
     """The packed quantize of the fast Hadamard kernels: exact .5 ties (scalar
     fallback), values far beyond +-qmax, near-zero rows and a non-finite row."""
