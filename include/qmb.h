@@ -263,6 +263,16 @@ int qmb_gemm_bench(int M, int N, int K, int mode, int iters, float* ms);
  * -> out [M, V] f32.  Tolerance-only (the reference's BLAS sums in its own order). */
 int qmb_lm_head(const float* x, int M, int K, const float* emb, int V, float* out, qmb_stream_t stream);
 
+/* The LM head above 8 rows on the fp16 tensor cores (model.py lm_head_split16, the
+ * two GEMMs by cuBLAS): qmb_lm_split16 scales each row of x [M, K] by a power of two
+ * s_r (max |x_r s_r| < 2^14) and splits it into fp16 halves, out16 [2M, K] = [hi; lo],
+ * inv_scale[r] = 1 / s_r; qmb_lm_combine16 forms out [M, V] =
+ * ((p[r] + p[M + r]) + q[r]) * inv_scale[r] * 2^-k from p = [hi; lo] W_hi^T [2M, V] and
+ * q = hi W_lo^T [M, V] (W * 2^k = W_hi + W_lo). */
+int qmb_lm_split16(const float* x, int M, int K, void* out16, float* inv_scale, qmb_stream_t stream);
+int qmb_lm_combine16(const float* p, const float* q, const float* inv_scale, int M, int V, int k, float* out,
+                     qmb_stream_t stream);
+
 int qmb_embed_gather(const float* table, const long long* tokens, long long n, int D, float* out,
                      qmb_stream_t stream);
 

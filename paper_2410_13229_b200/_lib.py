@@ -86,6 +86,8 @@ PROTOTYPES = {
     "qmb_verify_math":(c_int, [c_int, c_int, c_vp, c_vp, c_vp]),
     "qmb_embed_gather": (c_int, [c_vp, c_vp, c_ll, c_int, c_vp, c_vp]),
     "qmb_lm_head": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_vp, c_vp]),
+    "qmb_lm_split16": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_vp]),
+    "qmb_lm_combine16": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_vp, c_vp]),
 }
 
 _lib = None

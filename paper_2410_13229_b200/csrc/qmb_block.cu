@@ -1093,3 +1093,16 @@ extern "C" int qmb_lm_head(const float* x, int M, int K, const float* emb, int V
   QMB_CUDA(lm_head(x, M, K, emb, V, out, (cudaStream_t)stream), "lm head");
   return 0;
 }
+
+extern "C" int qmb_lm_split16(const float* x, int M, int K, void* out16, float* inv_scale, qmb_stream_t stream) {
+  if (M < 0 || K <= 0 || (M && (!x || !out16 || !inv_scale))) return fail(QMB_E_ARG, "null argument");
+  QMB_CUDA(lm_split16(x, M, K, out16, inv_scale, (cudaStream_t)stream), "lm split16");
+  return 0;
+}
+
+extern "C" int qmb_lm_combine16(const float* p, const float* q, const float* inv_scale, int M, int V, int k,
+                                float* out, qmb_stream_t stream) {
+  if (M < 0 || V < 0 || (M && V && (!p || !q || !inv_scale || !out))) return fail(QMB_E_ARG, "null argument");
+  QMB_CUDA(lm_combine16(p, q, inv_scale, M, V, k, out, (cudaStream_t)stream), "lm combine16");
+  return 0;
+}

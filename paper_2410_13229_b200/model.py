@@ -110,9 +110,9 @@ class DeviceModel:
     def lm_head(self, final: torch.Tensor) -> torch.Tensor:
         """Tied f32 logits final @ embedding^T (model.py:257-258); tolerance-only
         against the reference's BLAS summation order.  Up to 8 rows: libqmb's
-        streaming f32 GEMV (the embedding read once); more rows: cuBLAS's f32 GEMM
-        (TF32 off) -- libqmb's FFMA2 tile kernel (qmb_lm_head) measured slower there
-        (B = 64: 464 vs 367 us), an f32 GEMM needs the tensor cores to do better."""
+        streaming f32 GEMV (the embedding read once); more rows: the split-fp16
+        tensor-core product (lm_head_split16) -- cuBLAS's f32 SIMT GEMM took 347 us
+        at B = 64, libqmb's FFMA2 tile kernel (qmb_lm_head) 464 us."""
         x = final.reshape(-1, self.D).contiguous()
         M = x.shape[0]
         if M <= 8:
@@ -120,12 +120,9 @@ class DeviceModel:
             _lib.check(self._lib.qmb_lm_head(x.data_ptr(), int(M), self.D, self.embedding.data_ptr(), self.V,
                                              out.data_ptr(), _device.stream_ptr()), "lm_head")
             return out.reshape(tuple(final.shape[:-1]) + (self.V,))
-        prev = torch.backends.cuda.matmul.allow_tf32
-        torch.backends.cuda.matmul.allow_tf32 = False
-        try:
-            return final @ self.embedding.T
-        finally:
-            torch.backends.cuda.matmul.allow_tf32 = prev
+        if getattr(self, "_emb16", None) is None:
+            self._emb16 = split16_weights(self.embedding)
+        return lm_head_split16(x, *self._emb16).reshape(tuple(final.shape[:-1]) + (self.V,))
 
     # ---------------------------------------------------------------- prefill
     def forward_hidden(self, tokens: torch.Tensor, *, states=None, scan_exp: int = 0, err=None):
@@ -252,6 +249,47 @@ class DeviceModel:
                     logits = self.decode_step(nxt, states, bufs=bufs)
         _device.err_flag().raise_if_set()
         return torch.cat(out, dim=1)
+
+
+def split16_weights(w: torch.Tensor):
+    """(w_hi, w_lo, k): w * 2^k = w_hi + w_lo + O(2^-22 |w|) with fp16 halves, 2^k a
+    power of two putting max |w| in [2^13, 2^14) (exact scaling, no fp16 overflow)."""
+    amax = float(w.abs().max()) if w.numel() else 0.0
+    k = 0 if not (amax > 0.0) or not torch.isfinite(torch.tensor(amax)) else 14 - int(torch.frexp(
+        torch.tensor(amax, dtype=torch.float64))[1])
+    ws = w.float() * (2.0 ** k)
+    hi = ws.half()
+    lo = (ws - hi.float()).half()
+    return hi.contiguous(), lo.contiguous(), k
+
+
+def lm_head_split16(x: torch.Tensor, w_hi: torch.Tensor, w_lo: torch.Tensor, k: int) -> torch.Tensor:
+    """f32 x [M, K] @ W^T [K, V] on the fp16 tensor cores: each row of x scaled by a
+    power of two below 2^14 and split x = x_hi + x_lo (fp16, libqmb qmb_lm_split16);
+    then x W^T ~ x_hi W_hi + x_lo W_hi + x_hi W_lo with f32 accumulation (cuBLAS, two
+    GEMMs over the weights: [x_hi; x_lo] W_hi^T and x_hi W_lo^T), combined and
+    unscaled by qmb_lm_combine16.  The dropped x_lo W_lo and the halves' own rounding
+    are ~2^-22 relative per product -- well inside the LM head's f32 tolerance
+    (1e-5 of the largest |logit|, tests/test_gpu_ops.py)."""
+    lib = _lib.load()
+    x = x.contiguous()
+    M, K = x.shape
+    V = w_hi.shape[0]
+    st = _device.stream_ptr()
+    x16 = torch.empty((2 * M, K), dtype=torch.float16, device=x.device)
+    inv = torch.empty((M,), dtype=torch.float32, device=x.device)
+    _lib.check(lib.qmb_lm_split16(x.data_ptr(), int(M), int(K), x16.data_ptr(), inv.data_ptr(), st), "lm_split16")
+    prev = torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction
+    torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
+    try:
+        p = torch.mm(x16, w_hi.T, out_dtype=torch.float32)
+        q = torch.mm(x16[:M], w_lo.T, out_dtype=torch.float32)
+    finally:
+        torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = prev
+    out = torch.empty((M, V), dtype=torch.float32, device=x.device)
+    _lib.check(lib.qmb_lm_combine16(p.data_ptr(), q.data_ptr(), inv.data_ptr(), int(M), int(V), int(k),
+                                    out.data_ptr(), st), "lm_combine16")
+    return out
 
 
 def device_model(model) -> DeviceModel:

@@ -297,3 +297,27 @@ def test_lm_head_tolerance(cuda, M, K, V):
     ref = (x.double() @ emb.double().T)
     err = float((out.double() - ref).abs().max())
     assert err <= 1e-5 * float(ref.abs().max()), err
+
+
+@pytest.mark.parametrize("M,K,V", [(64, 2560, 50280), (9, 768, 1000), (130, 100, 130)])
+def test_lm_head_split16_tolerance(cuda, M, K, V):
+    """The LM head above 8 rows (fp16-split tensor-core product, model.lm_head_split16)
+    against an f64 product: within 1e-5 of the largest |logit|, on rows of very
+    different magnitudes (the per-row power-of-two scaling), zero rows and tiny /
+    huge weights."""
+    from paper_2410_13229_b200.model import lm_head_split16, split16_weights
+
+    g = torch.Generator(device="cuda").manual_seed(M + K)
+    x = torch.randn((M, K), generator=g, device="cuda")
+    x[1] *= 1e4
+    x[2] *= 1e-6
+    x[3] = 0.0
+    emb = torch.randn((V, K), generator=g, device="cuda") * 0.05
+    emb[0] *= 1e-7
+    emb[1, :7] = 3.0
+    out = lm_head_split16(x, *split16_weights(emb))
+    ref = x.double() @ emb.double().T
+    for r in range(M):  # per row: the tolerance is relative to that row's largest logit
+        err = float((out[r].double() - ref[r]).abs().max())
+        assert err <= 1e-5 * float(ref[r].abs().max()) + 1e-30, (r, err)
+    assert not out[3].any()
