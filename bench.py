@@ -397,11 +397,20 @@ def run_ours(args):
         cur = tokens[:1, 0].contiguous()
         for _ in range(3):
             tpm.decode_step(cur, tstates)
-        ms_tp = _timed(lambda: tpm.decode_step(cur, tstates), max(10, args.steps * 4), stream, world, dev)
+        mode = "eager"
+        step = lambda: tpm.decode_step(cur, tstates)  # noqa: E731
+        if backend == "nccl":  # the whole step (collectives included) as one CUDA graph
+            try:
+                tgraph, ttok, _ = tpm.capture_decode(tstates)
+                ttok.copy_(cur)
+                step, mode = tgraph.replay, "CUDA graph"
+            except Exception as exc:  # (fall back to eager timing, say so)
+                mode = f"eager (graph capture failed: {type(exc).__name__})"
+        ms_tp = _timed(step, max(10, args.steps * 4), stream, world, dev)
         extras["tp_batch1_decode"] = {
             "value": 1.0 / (ms_tp * 1e-3), "unit": "tokens/s", "batch": 1, "tensor_parallel": world,
             "ms_per_token": ms_tp,
-            "note": "one sequence served by all N GPUs (channel-sharded blocks, eager, %s collectives)" % backend}
+            "note": "one sequence served by all N GPUs (channel-sharded blocks, %s, %s collectives)" % (mode, backend)}
         del tpm, tstates
         torch.cuda.empty_cache()
 

@@ -138,9 +138,10 @@ class DistComm:
 
     def all_gather_cols(self, ts: list) -> list:
         y = ts[0].contiguous()
-        parts = [torch.empty_like(y) for _ in range(self.world)]
-        self.dist.all_gather(parts, y, group=self.group)
-        return [torch.cat(parts, dim=1).contiguous()]
+        M, El = y.shape
+        flat = torch.empty((self.world * M, El), dtype=y.dtype, device=y.device)
+        self.dist.all_gather_into_tensor(flat, y, group=self.group)  # (one buffer: CUDA-graph capturable)
+        return [flat.view(self.world, M, El).permute(1, 0, 2).reshape(M, self.world * El).contiguous()]
 
 
 def tp_block_forward(shards: list, comm, u_q, B: int, T: int, outs: list, *, decode=False, states=None,
@@ -225,3 +226,26 @@ class TPModel:
     def decode_step(self, tokens: torch.Tensor, states) -> torch.Tensor:
         B = tokens.shape[0]
         return self.base.lm_head(self._run(tokens, B, 1, states, True))
+
+    def capture_decode(self, states):
+        """One decode step (every layer's four stages and three collectives, norms,
+        LM head) captured as a CUDA graph bound to `states`, as DeviceModel.capture_decode:
+        returns (graph, token_in [B] int64, logits_out [B, V]).  With DistComm the NCCL
+        collectives are captured too (warmed up first, outside the capture)."""
+        B = states[0][0][1].shape[0]
+        dev = _device.device()
+        tok = torch.zeros(B, dtype=torch.int64, device=dev)
+        scratch = self.new_states(B)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # lazy init (communicators, kernel attributes) outside the capture
+            self.decode_step(tok, scratch)
+            self.decode_step(tok, scratch)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        _device.err_flag().reset()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            logits = self.decode_step(tok, states)
+        graph._qmb_keep = scratch
+        return graph, tok, logits

@@ -102,3 +102,16 @@ def test_tp_model_bit_exact(cuda, G):
         b = tp.decode_step(cur, s_tp)
         assert np.array_equal(_bits(a), _bits(b))
         cur = a.argmax(-1)
+
+
+def test_tp_model_graph_nccl(cuda):
+    """The TP decode step with real NCCL collectives captured in a CUDA graph
+    (one rank: the single-GPU box), replays bit-identical to DeviceModel's decode."""
+    here = Path(__file__).resolve().parent
+    port = str(29700 + os.getpid() % 1000)
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=port)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+                        "--master-addr", "127.0.0.1", "--master-port", port, str(here / "tp_nccl_worker.py")],
+                       env=env, capture_output=True, text=True, timeout=600, cwd=str(here.parent))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "tp graph rank ok" in r.stdout, r.stdout[-2000:]
