@@ -375,6 +375,16 @@ static bool decode_scan_enabled() {
   return v;
 }
 
+// QMB_DECODE_SCAN2=0: decode from 16 sequences uses scan_tab16 (one thread per channel)
+// instead of the two-lane step kernel on dt_proj's codes.
+static bool decode_scan2_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("QMB_DECODE_SCAN2");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 static bool zsilu_in_gemm() {
   static const bool v = [] {
     const char* e = getenv("QMB_ZSILU_IN_GEMM");
@@ -681,6 +691,29 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     QMB_CUDA(gemm_i8(dtr, b->Rp, b->w_dt_t, b->Rp, (int)M, E, R, ep, st, 0, acc32), "dt_proj gemm");
     // scan + D skip + gate (qblock.py:207-210), gated y written over z
     PROF(4, st);
+    if (!tp && decode && b->exp_tab && zsilu_in_gemm() && decode_scan2_enabled() &&
+        decode_scan_ok(B, E, N, b->Nx, R, b->Rp)) {  // the two-lane step kernel on dt_proj's codes
+      DecodeScanParams dp{};
+      dp.x = scanx;
+      dp.ldx = b->Ep;
+      dp.z = z;
+      dp.bq = bq;
+      dp.cq = cq;
+      dp.delta = delta;
+      dp.ld_delta = E;
+      dp.lut_x = b->luts;
+      dp.lut_dt = b->luts + 256;
+      dp.lut_b = b->luts + 512;
+      dp.lut_c = b->luts + 768;
+      dp.exp_tab = b->exp_tab;
+      dp.d = b->d_deq;
+      dp.h = ssm_state;
+      dp.B = B;
+      dp.E = E;
+      dp.qmax = b->qmax;
+      dp.err = err;
+      QMB_CUDA(decode_scan(dp, st), "decode scan");
+    } else {
     ScanParams sp{};
     sp.x = scanx;
     sp.ldx = b->Ep;
@@ -723,6 +756,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     sp.fast = (scan_exp == 2 && !decode) ? 1 : 0;
     const int use_lut = scan_exp == 1 ? 0 : (decode ? decode_scan_mode() : 1);
     QMB_CUDA(selective_scan(sp, use_lut, st), "scan");
+    }
   }  // (unfused dt_proj + scan)
   }  // (unfused stages)
   if (stage == 2) {  // the local channels' gated y, all-gathered by the caller

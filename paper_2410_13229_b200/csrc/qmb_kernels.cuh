@@ -162,6 +162,7 @@ struct DecodeScanParams {
   float* z;                           // [B, E] silu(z) in, gated y out
   const int8_t* bq; const int8_t* cq; const int8_t* dtr; long long ld_dtr;  // x_proj outputs
   const int8_t* w_dt; long long ld_wdt; int R;  // [E, ld_wdt] dt_proj weights (K-major)
+  const int8_t* delta; long long ld_delta;       // non-null: dt_proj already ran, its codes [B, ld_delta]
   float dt_scale; const float* dt_bias; const float* qtab; float dt_div, dt_inv;
   const float* lut_x; const float* lut_dt; const float* lut_b; const float* lut_c;
   const float* exp_tab; const float* d;
