@@ -1411,6 +1411,18 @@ static cudaError_t launch_tc_choose(const int8_t* A, long long lda, const int8_t
                     N, ep);
 }
 
+// Fewest 256 x 256 pair tiles for which the CTA-pair kernel is used (QMB_PAIR_MIN).
+// Default 40: below one tile per SM pair the pair tile's doubled operand reuse still
+// beats a wave of 128 x 128 single-CTA tiles (2.8B out_proj at M = 1024, 40 pair
+// tiles: 36 vs 41 us); at 16-24 pair tiles it loses (130M out_proj 21 vs 18 us).
+static int pair_min_tiles() {
+  static const int v = [] {
+    const char* e = getenv("QMB_PAIR_MIN");
+    return e ? atoi(e) : 0;
+  }();
+  return v > 0 ? v : 40;
+}
+
 static bool gemm_spin() {
   static const bool v = [] {
     const char* e = getenv("QMB_GEMM_SPIN");
@@ -1465,7 +1477,7 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
     if (N <= 192) return launch_tc_choose<192>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
     const long long m_tiles = (M + TC_BM - 1) / TC_BM;
     // CTA pairs (256 x 256 tiles) once there are enough pair tiles for every SM pair
-    if (gemm_pair_enabled() && ((M + 255) / 256) * ((N + 255) / 256) >= num_sms() / 2)
+    if (gemm_pair_enabled() && ((M + 255) / 256) * ((N + 255) / 256) >= pair_min_tiles())
       return launch_tc_bn<256, 2>(A, lda, Bt, ldb, M, N, Kp, ep, st);
     if (m_tiles * ((N + 255) / 256) >= num_sms())
       return launch_tc_choose<256>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
