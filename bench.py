@@ -331,7 +331,7 @@ def run_ours(args):
 
     def step(tok):
         logits = dm.forward(tok, last_only=True)
-        nxt = torch.argmax(logits, dim=-1)
+        nxt = dm.argmax(logits)
         if world > 1:
             if shared:  # gloo dry run: host copies
                 parts = [torch.empty_like(nxt, device="cpu") for _ in range(world)]
@@ -501,8 +501,9 @@ def run_ours(args):
                 "comm": {"backend": backend, "world_size": world,
                          "dry_run_shared_gpu": shared, "collective": "all_gather_into_tensor of next-token ids"},
                 # ours per step: embed + 64 x (rmsnorm, in_proj, conv, x_proj, dt_proj, bc_dequant, scan,
-                # hadamard, out_proj) + final norm (the cuBLAS LM head and torch argmax are not counted)
-                "clocks": clk.summary(), "gpu_launches": 2 + 9 * cfg.n_layers,
+                # hadamard, out_proj) + final norm + LM-head split / combine + argmax (the LM head's two
+                # cuBLAS GEMMs are not counted)
+                "clocks": clk.summary(), "gpu_launches": 5 + 9 * cfg.n_layers,
                 "int8_peak_tops": peak_i8.value, "build_s": round(t_build, 1)}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -270,6 +270,11 @@ int qmb_lm_head(const float* x, int M, int K, const float* emb, int V, float* ou
  * ((p[r] + p[M + r]) + q[r]) * inv_scale[r] * 2^-k from p = [hi; lo] W_hi^T [2M, V] and
  * q = hi W_lo^T [M, V] (W * 2^k = W_hi + W_lo). */
 int qmb_lm_split16(const float* x, int M, int K, void* out16, float* inv_scale, qmb_stream_t stream);
+
+/* Greedy next tokens (model.py greedy decoding: numpy.argmax over the vocabulary):
+ * out[r] = the first index of the maximum of row r of logits [M, ld] over V columns,
+ * a NaN counting as the maximum (first NaN wins). */
+int qmb_argmax(const float* logits, int M, int V, long long ld, long long* out, qmb_stream_t stream);
 int qmb_lm_combine16(const float* p, const float* q, const float* inv_scale, int M, int V, int k, float* out,
                      qmb_stream_t stream);
 

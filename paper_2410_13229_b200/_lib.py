@@ -87,6 +87,7 @@ PROTOTYPES = {
     "qmb_embed_gather": (c_int, [c_vp, c_vp, c_ll, c_int, c_vp, c_vp]),
     "qmb_lm_head": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_vp, c_vp]),
     "qmb_lm_split16": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_vp]),
+    "qmb_argmax": (c_int, [c_vp, c_int, c_int, c_ll, c_vp, c_vp]),
     "qmb_lm_combine16": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_vp, c_vp]),
 }
 

@@ -1128,6 +1128,12 @@ extern "C" int qmb_lm_head(const float* x, int M, int K, const float* emb, int V
   return 0;
 }
 
+extern "C" int qmb_argmax(const float* logits, int M, int V, long long ld, long long* out, qmb_stream_t stream) {
+  if (M < 0 || V <= 0 || ld < V || (M && (!logits || !out))) return fail(QMB_E_ARG, "null argument");
+  QMB_CUDA(argmax_rows(logits, M, V, ld, out, (cudaStream_t)stream), "argmax");
+  return 0;
+}
+
 extern "C" int qmb_lm_split16(const float* x, int M, int K, void* out16, float* inv_scale, qmb_stream_t stream) {
   if (M < 0 || K <= 0 || (M && (!x || !out16 || !inv_scale))) return fail(QMB_E_ARG, "null argument");
   QMB_CUDA(lm_split16(x, M, K, out16, inv_scale, (cudaStream_t)stream), "lm split16");

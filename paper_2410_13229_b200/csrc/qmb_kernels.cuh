@@ -175,6 +175,7 @@ cudaError_t decode_scan(const DecodeScanParams& p, cudaStream_t st);
 
 // Tied LM head: out[M, V] = x[M, K] @ emb[V, K]^T, f32 (FFMA2 register-blocked GEMM).
 cudaError_t lm_head(const float* x, int M, int K, const float* emb, int V, float* out, cudaStream_t st);
+cudaError_t argmax_rows(const float* x, int M, int V, long long ld, long long* out, cudaStream_t st);
 cudaError_t lm_split16(const float* x, int M, int K, void* out16, float* inv, cudaStream_t st);
 cudaError_t lm_combine16(const float* p, const float* q, const float* inv, int M, int V, int k, float* out,
                          cudaStream_t st);

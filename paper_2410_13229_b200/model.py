@@ -227,6 +227,17 @@ class DeviceModel:
         graph._qmb_keep = (bufs, scratch)  # keep captured buffers alive with the graph
         return graph, tok, logits
 
+    def argmax(self, logits: torch.Tensor) -> torch.Tensor:
+        """Greedy next tokens on the device (numpy.argmax semantics: first index of
+        the maximum, NaN wins): [..., V] f32 -> [...] int64."""
+        x = logits.reshape(-1, logits.shape[-1])
+        if x.stride(-1) != 1:
+            x = x.contiguous()
+        out = torch.empty(x.shape[0], dtype=torch.int64, device=x.device)
+        _lib.check(self._lib.qmb_argmax(x.data_ptr(), int(x.shape[0]), int(x.shape[1]), int(x.stride(0)),
+                                        out.data_ptr(), _device.stream_ptr()), "argmax")
+        return out.reshape(logits.shape[:-1])
+
     def greedy_generate(self, prompt: torch.Tensor, steps: int, use_graph: bool = True) -> torch.Tensor:
         """Greedy decoding with carried state (quantized analogue of
         model.greedy_decode, model.py:364-379).  prompt [B, T] -> [B, T+steps].
@@ -238,7 +249,7 @@ class DeviceModel:
         else:
             bufs = self.decode_buffers(prompt.shape[0])
         for s in range(steps):
-            nxt = torch.argmax(logits, dim=-1)
+            nxt = self.argmax(logits)
             out.append(nxt[:, None])
             if s + 1 < steps:
                 if use_graph and steps > 1:

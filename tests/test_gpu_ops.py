@@ -321,3 +321,26 @@ def test_lm_head_split16_tolerance(cuda, M, K, V):
         err = float((out[r].double() - ref[r]).abs().max())
         assert err <= 1e-5 * float(ref[r].abs().max()) + 1e-30, (r, err)
     assert not out[3].any()
+
+
+def test_argmax_numpy_semantics(cuda):
+    """qmb_argmax == numpy.argmax per row: first index of the maximum (ties), a NaN
+    wins (first NaN), all -inf rows, strided rows."""
+    from paper_2410_13229_b200.model import DeviceModel
+
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((9, 50280)).astype(np.float32)
+    x[1, [5, 17, 40000]] = 9.0          # ties: first index
+    x[2, [100, 30000]] = np.nan         # first NaN
+    x[3, :] = -np.inf
+    x[4, :] = 0.0
+    x[5, -1] = 1e30                     # last column
+    x[6, 7] = np.inf
+    dm = DeviceModel.__new__(DeviceModel)
+    from paper_2410_13229_b200 import _lib
+    dm._lib = _lib.load()
+    xt = torch.from_numpy(x).cuda()
+    got = dm.argmax(xt).cpu().numpy()
+    assert np.array_equal(got, np.argmax(x, axis=-1)), (got, np.argmax(x, axis=-1))
+    big = torch.from_numpy(np.concatenate([x, x], axis=1)).cuda()[:, :50280]  # strided rows
+    assert np.array_equal(dm.argmax(big).cpu().numpy(), np.argmax(x, axis=-1))
