@@ -173,3 +173,33 @@ def _host_model(qm):
         layers.append(l2)
     h.layers = layers
     return h
+
+
+def test_2p8b_batch1_1k_bit_exact(cuda, s2p8b, oracle):
+    """BASELINE config 3 at batch 1: the 2.8B block over one 1024-token sequence --
+    in_proj on CTA-pair tiles (M = 1024), out_proj on the CTA-pair kernel from 40
+    pair tiles, the four-lane state-split scan -- every stage, the output, the final
+    state and conv window bit-exact with the oracle."""
+    import paper_2410_13229_b200  # noqa: F401
+    from paper_2410_13229_b200 import _device
+    from paper_2410_13229_b200.qblock import device_block
+
+    z, meta, qb, ob = s2p8b
+    c = meta["cfg"]
+    D, E, N, R = c["d_model"], c["d_inner"], c["d_state"], c["dt_rank"]
+    T = 1024
+    u = np.random.default_rng(1024).integers(-127, 128, size=(1, T, D)).astype(np.int8)
+    dev = device_block(qb)
+    ws = torch.zeros(dev.workspace_bytes(T), dtype=torch.uint8, device="cuda")
+    out = torch.empty((T, D), dtype=torch.float32, device="cuda")
+    conv, h = dev.new_state(1)
+    dev.prefill(torch.from_numpy(u[0]).cuda(), 1, T, out, u_scale=meta["u_scale"], conv_state_out=conv,
+                ssm_state_out=h, workspace=ws)
+    _device.err_flag().raise_if_set()
+    views = _stage_views(dev, ws, T, E, N, R)
+    ref = oracle.block_stages(u[0], meta["u_scale"], ob)
+    for stage, got in views.items():
+        assert np.array_equal(_bits(got), _bits(ref[stage])), stage
+    assert np.array_equal(_bits(out.cpu().numpy()), _bits(ref["out"]))
+    assert np.array_equal(_bits(h.cpu().numpy()[0]), _bits(ref["h"]))
+    assert np.array_equal(conv.cpu().numpy()[0], ref["conv_state"])
