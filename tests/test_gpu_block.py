@@ -125,12 +125,14 @@ def test_block_many_sequences_bit_exact(cuda, oracle, name, B, T):
 
 @pytest.mark.parametrize("name,B,T", [("m12_full", 1, 1), ("m12_full", 2, 2), ("m20_full", 3, 3), ("m20_full", 5, 47),
                                       ("m20_full", 2, 1000), ("p2_naive", 4, 16), ("p2_inper", 7, 33),
-                                      ("s130m", 1, 100), ("s130m", 15, 21), ("s2p8b", 2, 40), ("s2p8b", 4, 17)])
+                                      ("s130m", 1, 100), ("s130m", 1, 2048), ("s130m", 15, 21), ("s2p8b", 2, 40),
+                                      ("s2p8b", 4, 17)])
 def test_block_small_batch_bit_exact(cuda, oracle, name, B, T):
-    """B < 16 takes the state-split scan (4 lanes per channel, skewed one step
-    apart, the in-order acc sum handed lane to lane): ragged T (shorter than the
-    skew, not a multiple of the 16-step chunk, 1000 steps) and partial
-    sequence groups; outputs and final states bit-exact against the oracle."""
+    """B < 16 takes the state-split scan (2 lanes per channel, 4 for a single
+    sequence, skewed 4 steps apart, the in-order acc sum handed lane to lane): ragged
+    T (shorter than the skew, not a multiple of the 16-step chunk, 1000 steps, the
+    130M shape at BASELINE config 2's 2K tokens) and partial sequence groups; outputs
+    and final states bit-exact against the oracle."""
     from paper_2410_13229_b200 import _device
     from paper_2410_13229_b200.qblock import device_block
 
