@@ -385,6 +385,15 @@ static bool decode_scan2_enabled() {
   return v;
 }
 
+// QMB_CONV_FUSE=0: the decode conv step as its own kernel after the in_proj GEMV.
+static bool conv_fuse_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("QMB_CONV_FUSE");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 static bool zsilu_in_gemm() {
   static const bool v = [] {
     const char* e = getenv("QMB_ZSILU_IN_GEMM");
@@ -496,6 +505,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
 
   if (stage >= 3) return tp_back(b, tp, B, T, out, accum, err, st, acc32, M);
   bool fused_dscan = false;
+  bool conv_fused = false;
   // in_proj (qblock.py:192-198)
   PROF(0, st);
   if (stage != 2) {
@@ -519,6 +529,23 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     // z-half: silu(z) (the gate's factor, ssm.py:110-111) is computed here, in
     // the epilogue that overlaps the MMAs, instead of in the issue-bound scan.
     ep.seg[1] = EpiSeg{E, 2 * E, zsilu_in_gemm() ? EPI_F32_SILU : EPI_F32, s_lin, 1.0f, z, E, nullptr};
+    // decode through the GEMV: the conv step runs in its epilogue (one launch fewer)
+    conv_fused = !tp && decode && conv_fuse_enabled() && !decode_mid_enabled() &&
+                 gemv_selected(A, lda, b->w_in_t, b->Dp, (int)M, D);
+    if (conv_fused) {
+      EpiConv& cf = ep.cf;
+      cf.state = conv_state;
+      cf.w = b->conv_w;
+      cf.bias = b->conv_b;
+      cf.out = scanx;
+      cf.ldo = b->Ep;
+      cf.s_conv = f32(b->act[QMB_ACT_CONV_IN] * b->s_conv_w);
+      cf.s_out = f32(b->act[QMB_ACT_X]);
+      cf.inv_out = 1.0f / cf.s_out;
+      cf.thr = silu_quant_thr(cf.s_out, b->qmax, st);
+      cf.K = b->Kc;
+      cf.C = E;
+    }
     QMB_CUDA(gemm_i8(A, lda, b->w_in_t, b->Dp, (int)M, 2 * E, D, ep, st, 0, acc32), "in_proj gemm");
   }
   }  // (stage != 2)
@@ -594,7 +621,9 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
                        b->Rp, nullptr};
     QMB_CUDA(epi_apply_i32(tp->xacc, (int)M, b->Nx, ep, st), "x_proj finish");
   } else {
-  if (decode) {
+  if (decode && conv_fused) {
+    // (done in in_proj's GEMV epilogue)
+  } else if (decode) {
     QMB_CUDA(conv_step(xq, E, conv_state, b->conv_w, b->conv_b, scanx, b->Ep, B, E, b->Kc, s_conv,
                        f32(b->act[QMB_ACT_X]), b->qmax, err, st),
              "conv step");

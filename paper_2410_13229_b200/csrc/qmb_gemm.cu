@@ -786,6 +786,33 @@ __global__ void __launch_bounds__(256) gemm_i8_simt_kernel(const int8_t* __restr
 // same per-element code as every other path (epi_store_one).
 constexpr int GV_WC = 4;  // column warps per CTA (16 columns)
 
+// in_proj x column (row m, channel oc) -> its code, then the fused conv step (EpiConv)
+__device__ __forceinline__ void gemv_conv_x(const EpiParams& ep, const EpiSeg& sg, int m, int oc, int acc,
+                                            uint32_t& err) {
+  float v = __fmul_rn(__int2float_rn(acc), sg.acc_scale);
+  if (sg.bias) v = __fadd_rn(v, sg.bias[oc]);
+  const int q = quant_fast(v, sg.out_div, sg.out_inv, ep.qmax, err);  // = EPI_QUANT
+  const EpiConv& cf = ep.cf;
+  int8_t* st = cf.state + (long long)m * (cf.K - 1) * cf.C + oc;
+  int ca = 0;  // int8 x int8 -> int32: exact in any order
+  for (int k = 0; k + 1 < cf.K; ++k) ca += (int)cf.w[(long long)k * cf.C + oc] * (int)st[(long long)k * cf.C];
+  ca += (int)cf.w[(long long)(cf.K - 1) * cf.C + oc] * q;
+  float real = __fmul_rn(__int2float_rn(ca), cf.s_conv);
+  if (cf.bias) real = __fadd_rn(real, cf.bias[oc]);
+  float d;
+  int y = silu_quant_level(real, cf.inv_out, (float)ep.qmax + 1.0f, ep.qmax, &d);
+  if (!(d < cf.thr)) {
+    y = silu_quant_exact(real, cf.s_out, ep.qmax);
+    if (y == INT_MIN) {
+      err |= QMB_ERR_NONFINITE;
+      y = 0;
+    }
+  }
+  cf.out[(long long)m * cf.ldo + oc] = (int8_t)y;
+  for (int k = 0; k + 2 < cf.K; ++k) st[(long long)k * cf.C] = st[(long long)(k + 1) * cf.C];
+  if (cf.K > 1) st[(long long)(cf.K - 2) * cf.C] = (int8_t)q;
+}
+
 template <int MB, int WK>
 __global__ void __launch_bounds__(32 * GV_WC * WK) gemv_i8_kernel(const int8_t* __restrict__ A, long long lda,
                                                                  const int8_t* __restrict__ Bt, long long ldb, int M,
@@ -887,8 +914,12 @@ __global__ void __launch_bounds__(32 * GV_WC * WK) gemv_i8_kernel(const int8_t* 
       }
       uint32_t err = 0;
       int oc;
-      const EpiSeg sg = pick_seg(ep, epi_locate(ep, n0 + j, &oc));
-      epi_store_one(ep, sg, m, oc, v, err, qt);
+      const int s = epi_locate(ep, n0 + j, &oc);
+      const EpiSeg sg = pick_seg(ep, s);
+      if (ep.cf.state && s == 0)
+        gemv_conv_x(ep, sg, m, oc, v, err);
+      else
+        epi_store_one(ep, sg, m, oc, v, err, qt);
       flag_error(ep.err, err);
     }
   }
@@ -1439,6 +1470,10 @@ static bool gemv_enabled() {
   return v;
 }
 
+bool gemv_selected(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int Kp) {
+  return gemv_enabled() && gemv_ok(A, lda, Bt, ldb, M, Kp);
+}
+
 cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
                     const EpiParams& ep_in, cudaStream_t st, int force_path, int32_t* acc32, int* defer) {
   if (defer) *defer = 0;
@@ -1457,6 +1492,7 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
   int path = force_path;
   // decode-size M: the streaming GEMV (path 3); QMB_GEMV=0 keeps the tensor-core split-K path
   if (path == 0 && gemv_enabled() && gemv_ok(A, lda, Bt, ldb, M, Kp)) path = 3;
+  if (ep.cf.state && path != 3) return cudaErrorInvalidValue;  // (only the GEMV fuses the conv step)
   if (path == 3) {
     if (!gemv_ok(A, lda, Bt, ldb, M, Kp)) return cudaErrorInvalidValue;
     return launch_gemv(A, lda, Bt, ldb, M, N, Kp, ep, st);

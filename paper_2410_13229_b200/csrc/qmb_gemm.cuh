@@ -129,6 +129,20 @@ __device__ __forceinline__ int softplus_quant(float v, const float* __restrict__
   return q;
 }
 
+// Decode GEMV only: the causal conv step of fused_qconv (qblock.py:126-143) fused onto
+// in_proj's x columns.  Column i of row b: q = the x code; acc = sum_k w[k][i] x_k over
+// the carried window (state [B][K-1][C]) and q; out[b][i] = quantize(silu(f32(acc) *
+// s_conv + bias[i]), s_out); the window shifts by q.  state == nullptr: off.
+struct EpiConv {
+  int8_t* state;
+  const int8_t* w;      // [K][C] taps
+  const float* bias;    // [C] dequantized conv bias or nullptr
+  int8_t* out;          // [B][ldo] scan input codes
+  long long ldo;
+  float s_conv, s_out, inv_out, thr;
+  int K, C;
+};
+
 struct EpiParams {
   int nseg;
   int qmax;
@@ -146,6 +160,7 @@ struct EpiParams {
   int32_t* acc32;  // [splitk, M, N] int32 partials; a second kernel sums them and runs the epilogue
   int32_t* raw_out;  // non-null: the exact int32 sums go to raw_out[m * raw_ld + n] instead of any epilogue
   long long raw_ld;  // (single segment [0, N), no interleave; tensor-parallel partial products)
+  EpiConv cf;        // decode GEMV: conv step fused onto segment 0 (see EpiConv)
 };
 
 // Segment by value with compile-time indices only: a runtime index into the
@@ -224,6 +239,8 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
                     const EpiParams& ep, cudaStream_t st, int force_path /*0 auto, 1 tc, 2 simt, 3 gemv*/,
                     int32_t* acc32_scratch = nullptr, int* defer_splitk = nullptr);
 cudaError_t epi_apply_i32(const int32_t* acc, int M, int N, const EpiParams& ep, cudaStream_t st);
+// gemm_i8 will take the decode GEMV (the only path that honours EpiParams::cf)
+bool gemv_selected(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int Kp);
 // defer_splitk (nullable): when the launch splits K (skinny M with acc32_scratch), skip
 // the fix-up kernel and return the split count here (the int32 partials are left in
 // acc32_scratch as [split][M][N] for the caller's next kernel); 0 = the epilogue ran.
