@@ -531,7 +531,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     ep.seg[1] = EpiSeg{E, 2 * E, zsilu_in_gemm() ? EPI_F32_SILU : EPI_F32, s_lin, 1.0f, z, E, nullptr};
     // decode through the GEMV: the conv step runs in its epilogue (one launch fewer)
     conv_fused = !tp && decode && conv_fuse_enabled() && !decode_mid_enabled() &&
-                 gemv_selected(A, lda, b->w_in_t, b->Dp, (int)M, D);
+                 gemv_selected(A, lda, b->w_in_t, b->Dp, (int)M, 2 * E, D);
     if (conv_fused) {
       EpiConv& cf = ep.cf;
       cf.state = conv_state;
