@@ -89,7 +89,6 @@ struct qmb_block {
   int8_t* w_out_t;  // [D, Ep]
   float* luts;      // [4][256] dequant tables: x, dt, b, c (index q + 128)
   float* sp_qtab;   // [QTAB_FLOATS] verified softplus+quantize thresholds for dt_proj
-  unsigned* bar;    // [64] grid-barrier words of the fused decode kernel (zeroed at create)
 };
 
 extern "C" int qmb_abi_version(void) { return QMB_ABI_VERSION; }
@@ -233,7 +232,7 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
                o_wdt = take(w_dt_t.size()), o_dtb = take(E * 4), o_a = take((size_t)E * N * 4),
                o_acol = take((size_t)E * N), o_lut = take((size_t)128 * b->exp_ncols * 4), o_d = take(E * 4),
                o_wo = take(w_out_t.size()), o_luts = take(4 * 256 * 4), o_avals = take(a_vals.size() * 4),
-               o_qtab = take(QTAB_FLOATS * 4), o_scr = take(16), o_bar = take(256),
+               o_qtab = take(QTAB_FLOATS * 4), o_scr = take(16),
                o_etab = take(N == 16 ? (size_t)E * 128 * 16 * 4 : 0);
   cudaError_t e = cudaMalloc(&b->mem, off);
   if (e != cudaSuccess) {
@@ -256,7 +255,6 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
   b->luts = (float*)(base + o_luts);
   float* avals_dev = (float*)(base + o_avals);
   b->sp_qtab = (float*)(base + o_qtab);
-  b->bar = (unsigned*)(base + o_bar);
   uint32_t* scratch = (uint32_t*)(base + o_scr);
   struct Up {
     void* dst;
@@ -278,8 +276,7 @@ extern "C" int qmb_block_create(const qmb_block_desc* d, qmb_block** out) {
       return cuda_fail(e, "qmb_block_create: upload");
     }
   }
-  e = cudaMemset(b->bar, 0, 256);
-  if (e == cudaSuccess) e = build_exp_lut(b->luts + 256, avals_dev, b->exp_ncols, b->exp_lut, 0);
+  e = build_exp_lut(b->luts + 256, avals_dev, b->exp_ncols, b->exp_lut, 0);
   if (e == cudaSuccess && b->exp_tab) e = build_exp_tab(b->luts + 256, b->a_deq, E, b->exp_tab, 0);
   if (e == cudaSuccess) e = build_softplus_qtab(f32(d->act[QMB_ACT_DT]), b->qmax, b->sp_qtab, scratch, 0);
   // verified conv silu+quantize fast path for this layer's scale (cached)
@@ -354,18 +351,6 @@ static int decode_scan_mode() {
 
 // Where the gate's silu(z) is evaluated: the in_proj epilogue (default) or the
 // scan (QMB_ZSILU_IN_GEMM=0, kept for A/B measurements).  Same f32 values either way.
-// QMB_DECODE_MID=1 runs the decode middle (conv, x_proj, dt_proj, scan) as one
-// kernel with two grid barriers.  Bit-exact (tests run it), but measured slower
-// in CUDA-graph replay than the PDL-chained separate kernels (B = 64: 1.73 vs
-// 1.53 ms per 16 layers; B = 1: 0.72 vs 0.64 ms), so it is opt-in.
-static bool decode_mid_enabled() {
-  static const bool v = [] {
-    const char* e = getenv("QMB_DECODE_MID");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
 // QMB_DECODE_SCAN_FUSED=0 keeps dt_proj and the split-K fix-up as separate decode kernels.
 static bool decode_scan_enabled() {
   static const bool v = [] {
@@ -530,8 +515,8 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
     // the epilogue that overlaps the MMAs, instead of in the issue-bound scan.
     ep.seg[1] = EpiSeg{E, 2 * E, zsilu_in_gemm() ? EPI_F32_SILU : EPI_F32, s_lin, 1.0f, z, E, nullptr};
     // decode through the GEMV: the conv step runs in its epilogue (one launch fewer)
-    conv_fused = !tp && decode && conv_fuse_enabled() && !decode_mid_enabled() &&
-                 gemv_selected(A, lda, b->w_in_t, b->Dp, (int)M, 2 * E, D);
+    conv_fused = !tp && decode && conv_fuse_enabled() &&
+                 gemv_selected(A, lda, b->w_in_t, b->Dp, (int)M, D);
     if (conv_fused) {
       EpiConv& cf = ep.cf;
       cf.state = conv_state;
@@ -552,63 +537,7 @@ static int block_run(const qmb_block* b, const int8_t* u_q, double u_scale, int 
   // conv + SiLU + requant (qblock.py:199-201 -> fused_qconv :126-143)
   const float s_conv = f32(b->act[QMB_ACT_CONV_IN] * b->s_conv_w);
   PROF(1, st);
-  if (!tp && decode && b->exp_tab && zsilu_in_gemm() && decode_mid_enabled() &&
-      (long long)decode_mid_grid(E) * B * b->Nx <= SPLITK_SCRATCH_INTS && decode_mid_ok(B, E, N, b->Kc, b->Nx, R, b->Rp)) {
-    // conv step, x_proj, dt_proj + softplus, scan step and gate in one kernel
-    DecodeMidParams dp{};
-    dp.xq = xq;
-    dp.z = z;
-    dp.conv_state = conv_state;
-    dp.conv_w = b->conv_w;
-    dp.conv_b = b->conv_b;
-    dp.Kc = b->Kc;
-    dp.s_conv = s_conv;
-    dp.s_xo = f32(b->act[QMB_ACT_X]);
-    dp.inv_xo = 1.0f / dp.s_xo;
-    dp.thr_xo = silu_quant_thr(dp.s_xo, b->qmax, st);
-    dp.w_x = b->w_x_t;
-    dp.ld_wx = b->Ep;
-    dp.Nx = b->Nx;
-    EpiParams& ep = dp.epx;
-    ep.nseg = 3;
-    ep.qmax = b->qmax;
-    ep.err = err;
-    const double s_x = b->act[QMB_ACT_X];
-    ep.seg[0] = EpiSeg{0, N, EPI_QUANT, f32(s_x * b->s_w_b * 1.0), f32(b->act[QMB_ACT_B]), bq, N, nullptr};
-    ep.seg[1] = EpiSeg{N, 2 * N, EPI_QUANT, f32(s_x * b->s_w_c * 1.0), f32(b->act[QMB_ACT_C]), cq, N, nullptr};
-    ep.seg[2] = EpiSeg{2 * N, 2 * N + R, EPI_QUANT, f32(s_x * b->s_w_dtr * 1.0), f32(b->act[QMB_ACT_DT_R]), dtr,
-                       b->Rp, nullptr};
-    for (int k = 0; k < 3; ++k) ep.seg[k].out_inv = 1.0f / ep.seg[k].out_div;  // RN f32 reciprocal
-    dp.xpart = acc32;
-    dp.bq = bq;
-    dp.cq = cq;
-    dp.dtr = dtr;
-    dp.ld_dtr = b->Rp;
-    dp.w_dt = b->w_dt_t;
-    dp.ld_wdt = b->Rp;
-    dp.R = R;
-    dp.dt_scale = f32(b->act[QMB_ACT_DT_R] * b->s_w_dt * 1.0);
-    dp.dt_bias = b->dt_bias;
-    dp.qtab = b->sp_qtab;
-    dp.dt_div = f32(b->act[QMB_ACT_DT]);
-    dp.dt_inv = 1.0f / dp.dt_div;
-    dp.lut_x = b->luts;
-    dp.lut_dt = b->luts + 256;
-    dp.lut_b = b->luts + 512;
-    dp.lut_c = b->luts + 768;
-    dp.exp_tab = b->exp_tab;
-    dp.d = b->d_deq;
-    dp.h = ssm_state;
-    dp.bar = b->bar;
-    dp.B = B;
-    dp.E = E;
-    dp.qmax = b->qmax;
-    dp.err = err;
-    QMB_CUDA(decode_mid(dp, st), "decode middle");
-    PROF(2, st);
-    PROF(3, st);
-    PROF(4, st);
-  } else {
+  {
   if (stage == 2) {  // x_proj's requant from the all-reduced int32 sums
     EpiParams ep{};
     ep.nseg = 3;

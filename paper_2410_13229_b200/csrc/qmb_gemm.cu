@@ -825,11 +825,6 @@ __global__ void __launch_bounds__(32 * GV_WC * WK) gemv_i8_kernel(const int8_t* 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wc = warp % GV_WC, wk = warp / GV_WC;
   const int n0 = (blockIdx.x * GV_WC + wc) * 4;
-  // row block (skinny-N products at M > 8 run one row block of MB rows per grid row;
-  // every block re-reads the small weight matrix from L2)
-  const int m0 = blockIdx.y * MB;
-  A += (long long)m0 * lda;
-  M -= m0;
   const int nslices = Kp / 512 + ((Kp & 511) ? 1 : 0);
   const int per = (nslices + WK - 1) / WK;
   const int s0 = wk * per, s1 = min(nslices, s0 + per);
@@ -922,9 +917,9 @@ __global__ void __launch_bounds__(32 * GV_WC * WK) gemv_i8_kernel(const int8_t* 
       const int s = epi_locate(ep, n0 + j, &oc);
       const EpiSeg sg = pick_seg(ep, s);
       if (ep.cf.state && s == 0)
-        gemv_conv_x(ep, sg, m0 + m, oc, v, err);
+        gemv_conv_x(ep, sg, m, oc, v, err);
       else
-        epi_store_one(ep, sg, m0 + m, oc, v, err, qt);
+        epi_store_one(ep, sg, m, oc, v, err, qt);
       flag_error(ep.err, err);
     }
   }
@@ -934,47 +929,30 @@ template <int MB>
 static cudaError_t launch_gemv_mb(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N,
                                   int Kp, const EpiParams& ep, cudaStream_t st) {
   const int ctas = (N + 4 * GV_WC - 1) / (4 * GV_WC);
-  const int rblocks = (M + MB - 1) / MB;
   const int nslices = (Kp + 511) / 512;
-  // K split across warps when there are too few CTAs to keep every SM streaming
-  const int tot = ctas * rblocks;
-  int wk = (tot >= 2 * num_sms() || nslices < 2) ? 1 : (tot * 2 >= num_sms() || nslices < 4 ? 2 : 4);
-  if (const char* e = getenv("QMB_GEMV_WK")) wk = atoi(e) == 1 ? 1 : (atoi(e) == 2 ? 2 : (atoi(e) == 4 ? 4 : wk));
+  // K split across warps when there are too few column CTAs to keep every SM streaming
+  const int wk = (ctas >= 2 * num_sms() || nslices < 2) ? 1 : (ctas * 2 >= num_sms() || nslices < 4 ? 2 : 4);
   const size_t smem = (size_t)((MB * Kp + 15) & ~15) + (size_t)4 * 4 * GV_WC * MB * 4;
-  const dim3 grid((unsigned)ctas, (unsigned)rblocks);
   if (wk == 1) {
     cudaError_t e = ensure_smem_attr((const void*)gemv_i8_kernel<MB, 1>, smem);
     if (e != cudaSuccess) return e;
-    return launch_pdl(M <= 128, gemv_i8_kernel<MB, 1>, grid, dim3(32 * GV_WC), smem, st, A, lda, Bt, ldb, M, N, Kp,
-                      ep);
+    return launch_pdl(M <= 128, gemv_i8_kernel<MB, 1>, dim3((unsigned)ctas), dim3(32 * GV_WC), smem, st, A, lda, Bt,
+                      ldb, M, N, Kp, ep);
   }
   if (wk == 2) {
     cudaError_t e = ensure_smem_attr((const void*)gemv_i8_kernel<MB, 2>, smem);
     if (e != cudaSuccess) return e;
-    return launch_pdl(M <= 128, gemv_i8_kernel<MB, 2>, grid, dim3(64 * GV_WC), smem, st, A, lda, Bt, ldb, M, N, Kp,
-                      ep);
+    return launch_pdl(M <= 128, gemv_i8_kernel<MB, 2>, dim3((unsigned)ctas), dim3(64 * GV_WC), smem, st, A, lda, Bt,
+                      ldb, M, N, Kp, ep);
   }
   cudaError_t e = ensure_smem_attr((const void*)gemv_i8_kernel<MB, 4>, smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(M <= 128, gemv_i8_kernel<MB, 4>, grid, dim3(128 * GV_WC), smem, st, A, lda, Bt, ldb, M, N, Kp,
-                    ep);
+  return launch_pdl(M <= 128, gemv_i8_kernel<MB, 4>, dim3((unsigned)ctas), dim3(128 * GV_WC), smem, st, A, lda, Bt,
+                    ldb, M, N, Kp, ep);
 }
 
-// Skinny-N products (x_proj: N = dt_rank + 2 d_state) at 8 < M <= GV_MAX_ROWS run
-// the GEMV in row blocks of 8: one launch with the epilogue fused, where the
-// tensor-core path needs split-K over K = d_inner plus an int32 fix-up launch.
-// QMB_GEMV_SKINNY_N: the largest N taken this way (0: off).
-constexpr int GV_MAX_ROWS = 64;
-static int gemv_skinny_n() {
-  static const int v = [] {
-    const char* e = getenv("QMB_GEMV_SKINNY_N");
-    return e ? atoi(e) : 0;  // off by default: B = 16-64 decode measured within noise (1.219-1.257 vs 1.227 ms per 16 layers)
-  }();
-  return v;
-}
-
-static bool gemv_ok(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp) {
-  return M >= 1 && (M <= 8 || (M <= GV_MAX_ROWS && N <= gemv_skinny_n())) && Kp % 16 == 0 && lda % 16 == 0 && ldb % 16 == 0 && (uintptr_t)A % 16 == 0 &&
+static bool gemv_ok(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int Kp) {
+  return M >= 1 && M <= 8 && Kp % 16 == 0 && lda % 16 == 0 && ldb % 16 == 0 && (uintptr_t)A % 16 == 0 &&
          (uintptr_t)Bt % 16 == 0 && (size_t)8 * Kp <= 160 * 1024;
 }
 
@@ -1492,8 +1470,8 @@ static bool gemv_enabled() {
   return v;
 }
 
-bool gemv_selected(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp) {
-  return gemv_enabled() && gemv_ok(A, lda, Bt, ldb, M, N, Kp);
+bool gemv_selected(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int Kp) {
+  return gemv_enabled() && gemv_ok(A, lda, Bt, ldb, M, Kp);
 }
 
 cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp,
@@ -1513,10 +1491,10 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
                      Kp > 0;
   int path = force_path;
   // decode-size M: the streaming GEMV (path 3); QMB_GEMV=0 keeps the tensor-core split-K path
-  if (path == 0 && gemv_enabled() && gemv_ok(A, lda, Bt, ldb, M, N, Kp)) path = 3;
+  if (path == 0 && gemv_enabled() && gemv_ok(A, lda, Bt, ldb, M, Kp)) path = 3;
   if (ep.cf.state && path != 3) return cudaErrorInvalidValue;  // (only the GEMV fuses the conv step)
   if (path == 3) {
-    if (!gemv_ok(A, lda, Bt, ldb, M, N, Kp)) return cudaErrorInvalidValue;
+    if (!gemv_ok(A, lda, Bt, ldb, M, Kp)) return cudaErrorInvalidValue;
     return launch_gemv(A, lda, Bt, ldb, M, N, Kp, ep, st);
   }
   if (path == 0) path = (tc_ok && (M > 16 || acc32)) ? 1 : 2;

@@ -240,7 +240,7 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
                     int32_t* acc32_scratch = nullptr, int* defer_splitk = nullptr);
 cudaError_t epi_apply_i32(const int32_t* acc, int M, int N, const EpiParams& ep, cudaStream_t st);
 // gemm_i8 will take the decode GEMV (the only path that honours EpiParams::cf)
-bool gemv_selected(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int N, int Kp);
+bool gemv_selected(const int8_t* A, long long lda, const int8_t* Bt, long long ldb, int M, int Kp);
 // defer_splitk (nullable): when the launch splits K (skinny M with acc32_scratch), skip
 // the fix-up kernel and return the split count here (the int32 partials are left in
 // acc32_scratch as [split][M][N] for the caller's next kernel); 0 = the epilogue ran.

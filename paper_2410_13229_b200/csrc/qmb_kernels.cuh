@@ -117,44 +117,6 @@ cudaError_t build_exp_tab(const float* lut_dt, const float* a, int E, float* exp
 // exp_lut[r * ncols + c] = glibc_expf(lut_dt[r + 128] * a_vals[c]) for r in [0, 127]
 cudaError_t build_exp_lut(const float* lut_dt, const float* a_vals, int ncols, float* exp_lut, cudaStream_t st);
 
-// Fused decode middle of the block (conv step, x_proj, dt_proj + softplus, scan
-// step, gate) for T = 1: see decode_mid_kernel.
-struct DecodeMidParams {
-  const int8_t* xq;        // [B, E] in_proj x half (conv input codes)
-  float* z;                // [B, E] silu(z) in, gated y out
-  int8_t* conv_state;      // [B, Kc - 1, E] carried window (updated)
-  const int8_t* conv_w;    // [Kc, E]
-  const float* conv_b;     // [E] dequantized conv bias, or null
-  int Kc;
-  float s_conv, s_xo, inv_xo, thr_xo;  // conv acc scale, output scale / reciprocal, verified silu margin
-  const int8_t* w_x;       // [Nx, ld_wx] x_proj weights (rows b | c | dt_r, K-major)
-  long long ld_wx;
-  int Nx;
-  EpiParams epx;           // x_proj epilogue (3 requant segments -> bq, cq, dtr)
-  int32_t* xpart;          // [G, B, Nx] per-CTA partial sums (workspace), G = decode_mid_grid(E)
-  const int8_t* bq;        // [B, 16] (epx outputs)
-  const int8_t* cq;
-  const int8_t* dtr;       // [B, ld_dtr]
-  long long ld_dtr;
-  const int8_t* w_dt;      // [E, ld_wdt] dt_proj weights (K-major)
-  long long ld_wdt;
-  int R;
-  float dt_scale;          // f32(s_dtr * s_wdt)
-  const float* dt_bias;    // [E] dequantized, or null
-  const float* qtab;       // verified softplus+quantize thresholds
-  float dt_div, dt_inv;    // f32(act dt) and its RN reciprocal
-  const float* lut_x; const float* lut_dt; const float* lut_b; const float* lut_c;
-  const float* exp_tab;    // [E, 128, 16]
-  const float* d;          // [E]
-  float* h;                // [B, E, 16] carried state (updated)
-  unsigned* bar;           // 256 bytes in the block handle (grid barrier words 0 and 32)
-  int B, E, qmax;
-  uint32_t* err;
-};
-bool decode_mid_ok(int B, int E, int N, int Kc, int Nx, int R, int Rp);
-int decode_mid_grid(int E);  // CTAs (= partial rows of xpart)
-cudaError_t decode_mid(const DecodeMidParams& p, cudaStream_t st);
-
 // Decode scan with dt_proj fused (x_proj's b | c | dt_r codes as input): see
 // decode_scan_kernel.
 struct DecodeScanParams {

@@ -7,6 +7,8 @@ is tolerance-checked only.
 """
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -130,13 +132,50 @@ class DeviceModel:
         list (one (conv, h) pair per layer, shaped for B), the prefill writes
         the carried decode state into it."""
         B, T = tokens.shape
+        groups = prefill_groups(B, T)
+        if groups > 1 and states is None:
+            return self._forward_hidden_groups(tokens, groups, scan_exp, err)
+        return self._forward_hidden_one(tokens, states=states, scan_exp=scan_exp, err=err)
+
+    def _forward_hidden_groups(self, tokens, groups, scan_exp, err):
+        """Sequences are independent (model.py:306-320): the batch runs as `groups`
+        contiguous row groups, each through all layers on its own CUDA stream with
+        its own workspace, so one group's kernels fill the SMs another group's
+        kernel leaves idle in its last wave.  Each group's rows are computed by the
+        same kernels as a lone prefill of those sequences: bit-identical."""
+        B, T = tokens.shape
+        err = err if err is not None else _device.err_flag()
+        main = torch.cuda.current_stream()
+        if getattr(self, "_pf_streams", None) is None or len(self._pf_streams) < groups:
+            self._pf_streams = [torch.cuda.Stream() for _ in range(groups)]
+            self._pf_ws = [None] * groups
+        final = torch.empty((B * T, self.D), dtype=torch.float32, device=tokens.device)
+        bounds = [(g * B) // groups for g in range(groups + 1)]
+        for g in range(groups):
+            s = self._pf_streams[g]
+            s.wait_stream(main)
+            with torch.cuda.stream(s):
+                rows = tokens[bounds[g]:bounds[g + 1]]
+                need = max(b.workspace_bytes(rows.shape[0] * T) for b in self.blocks)
+                if self._pf_ws[g] is None or self._pf_ws[g].numel() < need:
+                    self._pf_ws[g] = torch.empty(need, dtype=torch.uint8, device=tokens.device)
+                self._forward_hidden_one(rows, scan_exp=scan_exp, err=err, ws=self._pf_ws[g],
+                                         out=final[bounds[g] * T:bounds[g + 1] * T])
+        for g in range(groups):
+            main.wait_stream(self._pf_streams[g])
+        final.record_stream(main)
+        return final
+
+    def _forward_hidden_one(self, tokens, *, states=None, scan_exp=0, err=None, ws=None, out=None):
+        B, T = tokens.shape
         M = B * T
         stream = _device.stream_ptr()
         err = err if err is not None else _device.err_flag()
         x_out = self.embed(tokens)
         x_res = torch.zeros_like(x_out)
         u_q = torch.empty((M, self.D), dtype=torch.int8, device=x_out.device)
-        ws = _device.workspace(max(b.workspace_bytes(M) for b in self.blocks))
+        if ws is None:
+            ws = _device.workspace(max(b.workspace_bytes(M) for b in self.blocks))
         # The residual stream lives in x_res: layer 0 forms res = emb + 0 (model.py:249-253);
         # every block then adds its output into x_res in out_proj's epilogue, which is the
         # next fused_rmsnorm_quant's `x_out + x_res` (qblock.py:181) - so later norms read
@@ -149,7 +188,7 @@ class DeviceModel:
             conv, h = states[li] if states is not None else (None, None)
             blk.prefill(u_q, B, T, x_res, conv_state_out=conv, ssm_state_out=h, scan_exp=scan_exp, workspace=ws,
                         err=err, stream=stream, accumulate=True)
-        final = torch.empty_like(x_out)
+        final = out if out is not None else torch.empty_like(x_out)
         self._rmsnorm(x_res, None, None, self.final_norm, 1.0, None, final, M, err, stream)
         return final
 
@@ -260,6 +299,17 @@ class DeviceModel:
                     logits = self.decode_step(nxt, states, bufs=bufs)
         _device.err_flag().raise_if_set()
         return torch.cat(out, dim=1)
+
+
+def prefill_groups(B: int, T: int) -> int:
+    """Row groups (CUDA streams) of a batched prefill.  Default: 2 from 32 sequences
+    (2.8B, B = 64 x T = 1024, 16 layers: 5.49-5.55 vs 5.54-5.61 ms per layer over three
+    interleaved pairs, `tools/prefill_streams.py`; 3-4 groups are slower: the
+    persistent GEMMs' CTAs that start late on SMs held by the other groups' kernels
+    stretch their static tile schedule); QMB_PREFILL_STREAMS overrides."""
+    env = os.environ.get("QMB_PREFILL_STREAMS")
+    g = int(env) if env else (2 if B >= 32 else 1)
+    return max(1, min(g, B))
 
 
 def split16_weights(w: torch.Tensor):

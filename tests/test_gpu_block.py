@@ -221,22 +221,6 @@ def test_block_accumulate_is_the_residual_add(cuda, name):
     assert np.array_equal(acc.cpu().numpy().view(np.uint32), (row.cpu().numpy() + res0[:B]).view(np.uint32))
 
 
-def test_fused_decode_middle_bit_exact(cuda):
-    """QMB_DECODE_MID=1 (opt-in): conv step, x_proj, dt_proj + softplus and the scan
-    step in one kernel with two grid barriers -- the decode-equals-prefill checks
-    rerun in a fresh process with it enabled."""
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
-
-    here = Path(__file__).resolve().parent
-    env = dict(os.environ, QMB_DECODE_MID="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", str(here / "test_gpu_block.py"),
-                        "-k", "decode_equals_prefill"], env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-
-
 def test_handle_rebuilt_when_block_is_recalibrated(cuda, oracle):
     """The device handle cached on a QuantizedBlock is rebuilt when its scales change
     (the reference's QuantizedBlock is a mutable dataclass, qblock.py:75-95)."""

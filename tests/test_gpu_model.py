@@ -47,6 +47,23 @@ def test_batched_prefill_last_logits(cuda, oracle):
         assert np.max(np.abs(last[b] - ref)) <= LOGIT_RTOL * np.max(np.abs(ref))
 
 
+@pytest.mark.parametrize("groups", ["1", "2", "3"])
+def test_grouped_prefill_bit_exact(cuda, oracle, monkeypatch, groups):
+    """Batched prefill as row groups on separate CUDA streams (model.prefill_groups):
+    every sequence's final hidden state equals the oracle's bit for bit."""
+    from paper_2410_13229_b200.model import device_model
+
+    z, meta = load_npz("model_tiny2.npz")
+    qm = mirror_model(z, meta)
+    om = oracle_model(z, meta)
+    rng = np.random.default_rng(11)
+    toks = rng.integers(0, meta["config"]["vocab_size"], size=(5, 24))
+    monkeypatch.setenv("QMB_PREFILL_STREAMS", groups)
+    hid = device_model(qm).forward_hidden(torch.from_numpy(toks).cuda()).cpu().numpy().reshape(5, 24, -1)
+    for b in range(5):
+        assert np.array_equal(hid[b], oracle.forward_hidden(om, toks[b]))
+
+
 def test_greedy_decode_matches_oracle(cuda, oracle):
     """Greedy decoding with carried state against the composed oracle:
     the oracle's greedy tokens are fed back (teacher forcing, so one near-tie cannot
