@@ -22,6 +22,11 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--scan-exp", type=int, default=0, help="0 exact (default), 2 fast mode")
     args = ap.parse_args()
+    import os
+
+    # the profiled range runs the batch as ONE row group, so ncu's per-launch captures
+    # have the same M as the per-stage event times below (model.prefill_groups)
+    os.environ["QMB_PREFILL_STREAMS"] = "1"
     import torch
 
     from paper_2410_13229_b200 import _device, _lib
