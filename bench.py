@@ -458,15 +458,28 @@ def run_ours(args):
     # measured DRAM traffic per launch (ncu --set full, tools/ncu_layer.sh -> profiles/), in the same
     # unit as `achieved` x seconds: bytes for HBM-bound kernels
     traffic = None
+    co_bounds = None
     try:
         tr = json.loads((ROOT / "profiles" / "dram_traffic.json").read_text())
         if dom in tr.get("kernels", {}):
-            traffic = tr["kernels"][dom]["dram_bytes"]
+            k = tr["kernels"][dom]
+            traffic = k["dram_bytes"]
+            # what else bounds it (same ncu capture): shared-memory wavefronts per SM-cycle
+            # (1 / clk / SM peak; the exact scan's expf table), issue slots, SMs active
+            if k.get("elapsed_cycles"):
+                sms = torch.cuda.get_device_properties(0).multi_processor_count
+                wf = k.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")
+                co_bounds = {
+                    "shared_wavefront_frac": (wf / (sms * k["elapsed_cycles"]) if wf else None),
+                    "issue_slots_busy_frac": (k["issue_slots_busy_pct"] / 100 if "issue_slots_busy_pct" in k else None),
+                    "sm_active_frac": (k["sm_active_cycles"] / k["elapsed_cycles"] if "sm_active_cycles" in k else None),
+                    "source": "ncu --set full of one launch (profiles/dram_traffic.json, tools/ncu_layer.sh)"}
     except Exception:
         pass
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"],
                 "peak": peak_i8.value if d["bound"] == "tensor" else hbm, "unit": d["unit"], "frac": d["frac"],
                 "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
+                "co_bounds": co_bounds,
                 "algorithmic_bytes": (work[dom][1] * 1e9 if d["bound"] == "hbm" else None),
                 "peak_source": ("measured tcgen05 kind::i8 probe (qmb_measure_i8_peak)" if d["bound"] == "tensor"
                                 else "MEASURED_PEAKS.json hbm_gbs"),

@@ -41,6 +41,25 @@ def parse(path):
     return out
 
 
+def parse_details(path):
+    """Elapsed / SM-active cycles and issue-slot utilisation from the details export:
+    what bounds a kernel that is neither at its DRAM nor its tensor roofline."""
+    want = {"Elapsed Cycles": "elapsed_cycles", "SM Active Cycles": "sm_active_cycles",
+            "Issue Slots Busy": "issue_slots_busy_pct", "SM Frequency": "sm_ghz"}
+    out = {}
+    rows = list(csv.reader(open(path)))
+    h = rows[0]
+    for r in rows[1:]:
+        d = dict(zip(h, r))
+        k = want.get(d.get("Metric Name"))
+        if k and k not in out:
+            try:
+                out[k] = float(d["Metric Value"].replace(",", ""))
+            except ValueError:
+                pass
+    return out
+
+
 def main(src, dst):
     res = {}
     for p in sorted(Path(src).glob("*.raw.csv")):
@@ -49,6 +68,9 @@ def main(src, dst):
             continue
         try:
             res[key] = parse(p)
+            det = p.with_name(p.name[: -len(".raw.csv")] + ".details.csv")
+            if det.exists():
+                res[key].update(parse_details(det))
         except Exception as e:  # noqa: BLE001
             print(f"skip {p}: {e}", file=sys.stderr)
     Path(dst).write_text(json.dumps({"source": "ncu --set full --clock-control none, one launch per kernel "
