@@ -308,7 +308,7 @@ def run_ours(args):
         dist.init_process_group(backend)
         assert dist.get_world_size() == world
     from paper_2410_13229_b200 import _device, _lib
-    from paper_2410_13229_b200.model import device_model
+    from paper_2410_13229_b200.model import device_model, prefill_groups
     from paper_2410_13229_b200.synthetic import CONFIGS, build_model
 
     lib = _lib.load()
@@ -513,10 +513,13 @@ def run_ours(args):
                 "e2e": e2e, "decode": decode, "extras": extras, "roofline": roofline, "cpu_baseline": cpu,
                 "comm": {"backend": backend, "world_size": world,
                          "dry_run_shared_gpu": shared, "collective": "all_gather_into_tensor of next-token ids"},
-                # ours per step: embed + 64 x (rmsnorm, in_proj, conv, x_proj, dt_proj, bc_dequant, scan,
-                # hadamard, out_proj) + final norm + LM-head split / combine + argmax (the LM head's two
-                # cuBLAS GEMMs are not counted)
-                "clocks": clk.summary(), "gpu_launches": 5 + 9 * cfg.n_layers,
+                # ours per step: per prefill row group (model.prefill_groups) embed + L x (rmsnorm, in_proj,
+                # conv, x_proj, dt_proj, bc_dequant, scan, hadamard, out_proj) + final norm; then LM-head
+                # split / combine (or the f32 GEMV at <= 8 rows) + argmax (the LM head's two cuBLAS GEMMs
+                # are not counted)
+                "clocks": clk.summary(),
+                "gpu_launches": prefill_groups(B, T) * (2 + 9 * cfg.n_layers) + (2 if B > 8 else 1) + 1,
+                "gpu_launches_unit": "per step",
                 "int8_peak_tops": peak_i8.value, "build_s": round(t_build, 1)}
         print(json.dumps(line), flush=True)
     if world > 1:
