@@ -1454,6 +1454,14 @@ static int pair_min_tiles() {
   return v > 0 ? v : 40;
 }
 
+static bool pair128_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("QMB_PAIR128");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 static bool gemm_spin() {
   static const bool v = [] {
     const char* e = getenv("QMB_GEMM_SPIN");
@@ -1513,8 +1521,21 @@ cudaError_t gemm_i8(const int8_t* A, long long lda, const int8_t* Bt, long long 
     if (N <= 192) return launch_tc_choose<192>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
     const long long m_tiles = (M + TC_BM - 1) / TC_BM;
     // CTA pairs (256 x 256 tiles) once there are enough pair tiles for every SM pair
-    if (gemm_pair_enabled() && ((M + 255) / 256) * ((N + 255) / 256) >= pair_min_tiles())
+    if (gemm_pair_enabled() && ((M + 255) / 256) * ((N + 255) / 256) >= pair_min_tiles()) {
+      // few waves of 256 x 256 pair tiles (short prefills) of an epilogue-bound GEMM (dt_proj's
+      // softplus, K = dt_rank): 256 x 128 tiles when they fill the last wave clearly better.
+      // B = 1 / 2 x T = 1024: dt_proj 23.5 -> 21.3 / 29.7 -> 27.2 us; in_proj and out_proj lose
+      // (46 -> 53 us, 50 -> 54 us: half-width tiles cost more than the wave balance gains),
+      // so they keep 256 x 256 (profiles/r02/pair128_ab.log; QMB_PAIR128=0: off)
+      bool heavy = false;
+      for (int s = 0; s < ep.nseg; ++s) heavy |= ep.seg[s].kind == EPI_SOFTPLUS_Q;
+      const long long slots = num_sms() / 2;
+      auto wave_eff = [&](long long t) { return (double)t / (double)(((t + slots - 1) / slots) * slots); };
+      const long long t256 = ((M + 255) / 256) * ((N + 255) / 256), t128 = ((M + 255) / 256) * ((N + 127) / 128);
+      if (heavy && pair128_enabled() && wave_eff(t128) > wave_eff(t256) + 0.1)
+        return launch_tc_bn<128, 2>(A, lda, Bt, ldb, M, N, Kp, ep, st);
       return launch_tc_bn<256, 2>(A, lda, Bt, ldb, M, N, Kp, ep, st);
+    }
     if (m_tiles * ((N + 255) / 256) >= num_sms())
       return launch_tc_choose<256>(A, lda, Bt, ldb, M, N, Kp, ep, st, acc32, defer);
     if (m_tiles * ((N + 127) / 128) >= num_sms())
